@@ -1,0 +1,428 @@
+#!/usr/bin/env python
+"""bench.py -- throughput of the function blocks of arXiv 2004.09883 on B200 (driver contract).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl fb|reference] [--workload W]
+
+One JSON line on rank 0.  Headline workload (N=1): BASELINE configs[1], the paper-shaped
+Fourier-transform block: a forward complex 2D FFT of one 2048x2048 complex64 batch
+("grid size 2048*2048").  The matrix block (configs[2], 2048^3 GEMM in FP32
+3xTF32 and FP64) is measured in the same run and reported under "blocks" with its own
+roofline; so are the 256^2 forward+inverse (configs[0]) and the single-GPU 16384^2 FFT
+(the scaling baseline for configs[3]).  With N>1 ranks (torchrun) the headline is
+configs[3]: the slab-sharded 16384^2 FFT with its NCCL all-to-all (strong scaling).
+
+Timing: inputs resident in HBM; before every timed step L2 is flushed by a 512 MiB memset
+(untimed); each step is bracketed by CUDA events on the launching stream; barrier +
+synchronize around the timed region; max over ranks.  FLOP conventions: FFT 5 N log2 N
+(N = n0 n1), GEMM 2 M N K.  The `--impl reference` arm times the CPU oracle (oracle/) on a
+bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "2D FFT GFLOP/s & GEMM TFLOP/s at 1/2/4/8 B200; % of HBM/TC roofline"
+FLUSH_BYTES = 512 << 20
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return {"hbm_gbs": float(d["hbm_gbs"]), "bf16_tflops": float(d["bf16_tflops"]),
+                "bf16_tflops_sustained": float(d.get("bf16_tflops_sustained", d["bf16_tflops"])),
+                "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback (B200_PROFILING.md)"}
+
+
+def ncu_traffic(kernel: str, workload: str):
+    """dram bytes per launch from a committed `ncu --set full` summary, if present."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    d = json.load(open(p))
+    v = d.get(workload, {}).get(kernel)
+    return None if v is None else float(v)
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        time.sleep(0.25)
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 8:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx = float(f[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[4:8]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm.sort()
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- timing helpers
+def timed_steps(torch, fn, steps, warmup, flush, stream, dist=None):
+    """W untimed warm-ups, then exactly K steps; per-step CUDA events on `stream`, L2 flushed
+    (untimed) before each.  Returns per-step ms list (max over ranks of the mean applied by caller)."""
+    with torch.cuda.stream(stream):
+        for _ in range(warmup):
+            flush()
+            fn()
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in evs:
+            flush()
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+    return [a.elapsed_time(b) for a, b in evs]
+
+
+def max_over_ranks(torch, dist, v):
+    if dist is None:
+        return v
+    t = torch.tensor([v], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def fft_flops(n0, n1):
+    n = n0 * n1
+    return 5.0 * n * math.log2(n) if n > 1 else 0.0
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """--impl reference: the CPU oracle timed as the reference arm (no GPU work)."""
+    import numpy as np
+
+    import oracle
+    import synth
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    n = 2048
+    x = synth.complex_field(n, n)
+    cols_per_step = 16
+    threads = oracle.threads(0)
+    flop_equiv = fft_flops(n, n) * cols_per_step / n
+
+    def step(i):
+        for j in range(cols_per_step):
+            oracle.dft2d_col(x, (i * cols_per_step + j) % n)
+
+    for i in range(args.warmup):
+        step(i)
+    ts = []
+    for i in range(args.steps):
+        t0 = time.perf_counter()
+        step(i)
+        ts.append(time.perf_counter() - t0)
+    ms = 1e3 * float(np.mean(ts))
+    val = flop_equiv / (ms * 1e-3) / 1e9
+    sample = (f"{cols_per_step} full output columns of the 2048x2048 forward 2D DFT per step "
+              f"(naive O(n^2) definition, FP64), scaled to the 5 N log2 N flop count of the full transform")
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "GFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak" if args.gpus > 1 else "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": "fft2d_2048x2048_fwd", "n0": n, "n1": n},
+            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- fb arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="fb", choices=["fb", "reference"])
+    ap.add_argument("--no-extras", action="store_true", help="headline only (no blocks / cpu baseline / e2e)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--only", default="", help="comma list of blocks to run (debug)")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+
+    import paper_2004_09883_b200 as fb
+    import synth
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fb.fb_init(local)
+    stream = torch.cuda.Stream()
+    pk = peaks()
+    flush_buf = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+
+    def flush():
+        flush_buf.zero_()
+
+    only = set(filter(None, args.only.split(",")))
+    out = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "higher_is_better": True, "vs_baseline": None, "dtype": "f32", "data": "synthetic"}
+    blocks = {}
+
+    # ------------------------------------------------------------------ N = 1 headline: 2048^2 FFT
+    if world == 1:
+        n = 2048
+        x_h = synth.complex_field(n, n)
+        x = torch.from_numpy(x_h).cuda()
+        y = torch.empty_like(x)
+        L0 = fb.launch_count()
+        with ClockSampler(local) as clk:
+            ms = timed_steps(torch, lambda: fb.fb_fft2d(x, y, None, stream), args.steps, args.warmup, flush, stream)
+        launches = (fb.launch_count() - L0) // (args.steps + args.warmup)
+        t = float(np.mean(ms))
+        gflops = fft_flops(n, n) / (t * 1e-3) / 1e9
+        # dominant kernel: fft_pass_kernel (2 launches per step: row pass, column pass); each
+        # launch reads and writes the 32 MiB array once -> 64 MiB algorithmic bytes per launch.
+        bytes_launch = 2 * 8 * n * n
+        achieved = bytes_launch / ((t / launches) * 1e-3) / 1e9
+        out.update({"value": gflops, "unit": "GFLOP/s", "ms_per_step": t, "scaling": "strong",
+                    "config": {"workload": "fft2d_2048x2048_fwd", "n0": n, "n1": n, "element": "complex64",
+                               "l2": "flushed (512 MiB memset, untimed) before every timed step",
+                               "configs_index": 1},
+                    "roofline": {"bound": "hbm", "kernel": "fft_pass_kernel (row pass + column pass)",
+                                 "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                 "frac": achieved / pk["hbm_gbs"],
+                                 "traffic": ncu_traffic("fft_pass_kernel", "fft2d_2048"),
+                                 "algorithmic_bytes_per_launch": bytes_launch,
+                                 "launches_per_step": launches, "peak_source": pk["source"]},
+                    "gpu_launches": launches * args.steps, "clocks": clk.summary()})
+
+        # e2e through the public host API: pinned host in -> H2D -> FFT -> D2H -> pinned host out
+        if not args.no_extras:
+            xh = torch.from_numpy(x_h).pin_memory()
+            yh = torch.empty_like(xh).pin_memory()
+            for _ in range(args.warmup):
+                fb.fb_fft2d_host(xh, yh, stream=stream)
+            ets = []
+            for _ in range(args.steps):
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                flush()
+                a.record(stream)
+                fb.fb_fft2d_host(xh, yh, stream=stream)
+                b.record(stream)
+                torch.cuda.synchronize()
+                ets.append(a.elapsed_time(b))
+            te = float(np.mean(ets))
+            out["e2e"] = {"value": fft_flops(n, n) / (te * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": te,
+                          "h2d_bytes_per_step": int(xh.numel() * 8), "d2h_bytes_per_step": int(yh.numel() * 8),
+                          "api": "fb_fft2d_host (pinned host buffers)"}
+
+        # CPU oracle baseline on the same input: the full 2048^2 definition (~10-30 s)
+        if not (args.no_extras or args.no_cpu_baseline):
+            import oracle
+            thr = oracle.threads(0)
+            t0 = time.perf_counter()
+            ref = oracle.dft2d(x_h, nthreads=thr)
+            tcpu = time.perf_counter() - t0
+            err = oracle.rel_l2(y.cpu().numpy(), ref)
+            out["cpu_baseline"] = {"value": fft_flops(n, n) / tcpu / 1e9, "unit": "GFLOP/s", "cores": thr,
+                                   "kind": "oracle", "seconds": tcpu,
+                                   "sample": "the full 2048x2048 forward 2D DFT (naive O(n^2) per line, FP64) "
+                                             "on the bench input, flops counted as 5 N log2 N"}
+            out["parity"] = {"fft2d_2048_rel_l2_vs_oracle": err, "bar": 1e-5 * math.log2(n * n)}
+
+        if not args.no_extras:
+            blocks.update(extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only))
+    else:
+        out.update(run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, local))
+
+    if blocks:
+        out["blocks"] = blocks
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
+    res = {}
+    steps = max(3, args.steps // 2)
+
+    def want(k):
+        return not only or k in only
+
+    # configs[2]: GEMM 2048^3 FP32 (3xTF32 tcgen05) and FP64 (DMMA)
+    n = 2048
+    if want("gemm_f32_2048"):
+        A = torch.from_numpy(synth.real_matrix(n, n, synth.TID_GEMM_A)).cuda()
+        B = torch.from_numpy(synth.real_matrix(n, n, synth.TID_GEMM_B)).cuda()
+        C = torch.empty(n, n, device="cuda")
+        ws = torch.empty(fb.matmul_workspace_bytes(fb.FB_F32, n, n, n), dtype=torch.uint8, device="cuda")
+        ms = timed_steps(torch, lambda: fb.fb_matmul(A, B, C, ws, stream), steps, args.warmup, flush, stream)
+        t = float(np.mean(ms))
+        # the tensor-core kernel alone (operands pre-split)
+        kp = (n + 3) // 4 * 4
+        Ah = torch.empty(n, kp, device="cuda")
+        Al = torch.empty_like(Ah)
+        Bh = torch.empty(n, kp, device="cuda")
+        Bl = torch.empty_like(Bh)
+        fb.fb_tf32_split(A, Ah, Al, False, stream)
+        fb.fb_tf32_split(B, Bh, Bl, True, stream)
+        mk = timed_steps(torch, lambda: fb.fb_matmul_3xtf32_presplit(Ah, Al, Bh, Bl, C, stream), steps,
+                         args.warmup, flush, stream)
+        tk = float(np.mean(mk))
+        flops = 2.0 * n * n * n
+        tf32_peak = pk["bf16_tflops"] / 2.0  # TF32 dense = 1/2 of BF16 (guide's nominal ratio)
+        res["gemm_f32_2048"] = {
+            "value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
+            "config": {"workload": "gemm_2048^3_fp32_3xtf32", "configs_index": 2},
+            "roofline": {"bound": "tensor", "kernel": "gemm_3xtf32_kernel", "kernel_ms": tk,
+                         "achieved": 3 * flops / (tk * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
+                         "frac": 3 * flops / (tk * 1e-3) / 1e12 / tf32_peak,
+                         "note": "achieved counts the 3 TF32 MMAs (6MNK); useful 2MNK = achieved/3",
+                         "peak_source": pk["source"] + " bf16 x 0.5 (TF32/BF16 nominal ratio)"}}
+        del A, B, C, ws, Ah, Al, Bh, Bl
+    if want("gemm_f64_2048"):
+        A = torch.from_numpy(synth.real_matrix(n, n, synth.TID_GEMM_A, dtype=np.float64)).cuda()
+        B = torch.from_numpy(synth.real_matrix(n, n, synth.TID_GEMM_B, dtype=np.float64)).cuda()
+        C = torch.empty(n, n, device="cuda", dtype=torch.float64)
+        ms = timed_steps(torch, lambda: fb.fb_matmul(A, B, C, None, stream), steps, args.warmup, flush, stream)
+        t = float(np.mean(ms))
+        flops = 2.0 * n * n * n
+        f64_peak = pk["bf16_tflops"] / 2250.0 * 40.0  # B200 nominal FP64 tensor 40 TF vs 2250 TF bf16
+        res["gemm_f64_2048"] = {
+            "value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
+            "config": {"workload": "gemm_2048^3_fp64_dmma", "configs_index": 2},
+            "roofline": {"bound": "tensor", "kernel": "gemm_f64_dmma_kernel", "achieved": flops / (t * 1e-3) / 1e12,
+                         "peak": f64_peak, "unit": "TFLOP/s", "frac": flops / (t * 1e-3) / 1e12 / f64_peak,
+                         "peak_source": pk["source"] + " bf16 x 40/2250 (FP64/BF16 nominal ratio)"}}
+        del A, B, C
+    # configs[0]: 256^2 forward + inverse
+    if want("fft2d_256_fwd_inv"):
+        m = 256
+        x = torch.from_numpy(synth.complex_field(m, m)).cuda()
+        y = torch.empty_like(x)
+        z = torch.empty_like(x)
+
+        def fi():
+            fb.fb_fft2d(x, y, None, stream)
+            fb.fb_ifft2d(y, z, None, stream)
+        ms = timed_steps(torch, fi, steps, args.warmup, flush, stream)
+        t = float(np.mean(ms))
+        res["fft2d_256_fwd_inv"] = {"value": 2 * fft_flops(m, m) / (t * 1e-3) / 1e9, "unit": "GFLOP/s",
+                                    "ms_per_step": t, "config": {"workload": "fft2d_256x256_fwd+inv",
+                                                                 "configs_index": 0}}
+    # single-GPU 16384^2 forward: the N=1 point of the configs[3] scaling series
+    if want("fft2d_16384"):
+        m = 16384
+        x = torch.from_numpy(synth.complex_field(m, m)).cuda()
+        y = torch.empty_like(x)
+        ws = torch.empty(fb.lib().fb_fft2d_workspace_bytes(m, m), dtype=torch.uint8, device="cuda")
+        ms = timed_steps(torch, lambda: fb.fb_fft2d(x, y, ws, stream), steps, args.warmup, flush, stream)
+        t = float(np.mean(ms))
+        passes = 3  # row pass + two four-step column passes
+        ach = passes * 2 * 8 * m * m / (t * 1e-3) / 1e9
+        res["fft2d_16384"] = {"value": fft_flops(m, m) / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
+                              "config": {"workload": "fft2d_16384x16384_fwd_1gpu", "configs_index": 3},
+                              "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                           "frac": ach / pk["hbm_gbs"],
+                                           "note": f"{passes} HBM passes x (R+W) of the 2 GiB array"}}
+        del x, y, ws
+    return res
+
+
+def run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, local):
+    """configs[3]: 16384^2 FFT slab-sharded over `world` ranks, one NCCL all-to-all."""
+    n = 16384
+    rows = n // world
+    x = torch.from_numpy(synth.complex_field(n, n, row0=rank * rows, rows=rows)).cuda()
+    y = torch.empty(n, n // world, dtype=torch.complex64, device="cuda")
+    comm = fb.Comm(rank, world, local)
+    ws = torch.empty(fb.lib().fb_fft2d_slab_workspace_bytes(world, n, n), dtype=torch.uint8, device="cuda")
+    L0 = fb.launch_count()
+    with ClockSampler(local) as clk:
+        ms = timed_steps(torch, lambda: comm.fb_fft2d_slab(x, y, n, n, ws, stream), args.steps, args.warmup, flush,
+                         stream, dist)
+    launches = (fb.launch_count() - L0) // (args.steps + args.warmup)
+    t = max_over_ranks(torch, dist, float(np.mean(ms)))
+    comm.destroy()
+    val = fft_flops(n, n) / (t * 1e-3) / 1e9
+    hbm = 3 * 2 * 8 * n * n / world  # 3 local passes (row, 2 four-step column passes), R+W
+    ach = hbm / (t * 1e-3) / 1e9
+    return {"value": val, "unit": "GFLOP/s", "ms_per_step": t, "scaling": "strong",
+            "config": {"workload": "fft2d_16384x16384_slab_alltoall", "n0": n, "n1": n, "configs_index": 3,
+                       "parallelism": f"slab{world}",
+                       "l2": "inputs (2 GiB total) larger than L2; L2 also flushed before every step"},
+            "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": ach / pk["hbm_gbs"], "note": "per-GPU local HBM passes only; NCCL not counted"},
+            "gpu_launches": launches * args.steps + args.steps, "clocks": clk.summary()}
+
+
+if __name__ == "__main__":
+    sys.exit(main())

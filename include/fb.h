@@ -1,0 +1,174 @@
+/* fb.h -- C ABI of libfb.so: the two "function blocks" of Yamato, "Proposal of Automatic
+ * Offloading for Function Blocks of Applications" (arXiv 2004.09883), rebuilt for B200
+ * (sm_100a).  PAPER.md (P:n = line n) names the blocks; BASELINE.json's north_star fixes
+ * their semantics; DESIGN.md lists every reading taken where the paper is silent.
+ *
+ *   Fourier-transform block  ("grid size 2048*2048", replaced by
+ *                             cuFFT)                        -> fb_fft2d / fb_ifft2d
+ *   Matrix-calculation block ("linear algebra ... cuBLAS"; GEMM per the
+ *                             north_star, reading R9) -> fb_matmul
+ *   Interface with the host program (C-1: "the replacement library ... is installed
+ *   ... and a host (CPU) program is connected"; P:43 transfer overhead)
+ *                                                           -> fb_*_host variants
+ *   Multi-GPU partitioning (north_star (4)) -> fb_comm_*, fb_fft2d_slab, fb_matmul_rowblock
+ *
+ * Conventions (all entry points)
+ *   - Every parameter is a plain pointer or integer; there are no CUDA or torch types.
+ *     `stream` is a cudaStream_t passed as void* (NULL = the legacy default stream).
+ *   - Device pointers are owned by the caller.  The library never allocates or frees
+ *     caller-visible memory; it keeps only immutable per-device state (a 16384-entry FP32
+ *     twiddle table and a TMA descriptor scratch), created by fb_init (or lazily, on the
+ *     first call on a device, outside any stream capture).
+ *   - All work is enqueued on `stream`; no call synchronises the host except fb_init,
+ *     fb_comm_init/destroy and the *_host variants (which return after the D2H copy).
+ *   - Layout: row-major.  complex64 = {float re, im} interleaved (== torch.complex64).
+ *   - Validation happens before anything is enqueued; on error NOTHING is enqueued and a
+ *     status != FB_OK is returned, with a thread-local message in fb_last_error_detail().
+ *     Asynchronous device faults surface at the caller's next synchronisation.
+ *   - Determinism: for a fixed (shape, world size, build) every result is bitwise
+ *     reproducible run to run (no atomics in any reduction, no split-K).
+ */
+#ifndef FB_H
+#define FB_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    FB_OK = 0,
+    FB_ERR_INVALID_VALUE = 1,    /* null pointer, bad flag, partial overlap, n % P != 0 ... */
+    FB_ERR_UNSUPPORTED_SIZE = 2, /* FFT length not a power of two or > 2^14 */
+    FB_ERR_MISALIGNED = 3,       /* pointer not 16-byte aligned / leading dim breaks TMA rule */
+    FB_ERR_WORKSPACE = 4,        /* workspace pointer null or smaller than *_workspace_bytes */
+    FB_ERR_NOT_INITIALIZED = 5,  /* fb_comm_* on a null or destroyed communicator */
+    FB_ERR_CUDA = 6,             /* a CUDA runtime call or kernel launch failed */
+    FB_ERR_NCCL = 7,             /* an NCCL call failed (detail from ncclGetLastError) */
+    FB_ERR_ARCH = 8              /* device is not sm_100 (the kernels are sm_100a only) */
+} fb_status;
+
+typedef enum { FB_F32 = 0, FB_F64 = 1 } fb_dtype;
+
+/* Library version (major*10000 + minor*100 + patch). */
+int fb_version(void);
+/* Static string for a status code. */
+const char* fb_status_string(int status);
+/* Thread-local detail of the last error returned on this thread ("" if none). */
+const char* fb_last_error_detail(void);
+/* Number of kernels libfb has launched in this process (all devices).  Lets a harness
+ * count the library's own launches inside a timed region. */
+uint64_t fb_launch_count(void);
+
+/* Once per device: checks sm_100, builds the twiddle table W[j] = exp(-2 pi i j/16384)
+ * (computed in FP64 with sincospi, RN-rounded to FP32; exact at multiples of pi/2),
+ * resolves cuTensorMapEncodeTiled.  Synchronous.  Idempotent. */
+fb_status fb_init(int device);
+
+/* ------------------------------------------------------------------ Fourier block
+ * Y = DFT2(X) over an n0 x n1 complex64 array (n0 rows, n1 contiguous columns):
+ *   Y[k0,k1] = sum_{t0,t1} X[t0,t1] exp(-2 pi i (k0 t0/n0 + k1 t1/n1))      (unscaled)
+ * fb_ifft2d: sign +1 and the factor 1/(n0 n1) (exact: a power of two).
+ * Reading R1 (sign -1 forward, cuFFT/numpy convention), R2 (inverse scaled), R3 (layout),
+ * R4 (sizes): n0, n1 powers of two, 1 <= n <= 16384.
+ * x and y: device pointers, 16-byte aligned, n0*n1*8 bytes each; x == y (in place) is
+ * allowed, partial overlap is FB_ERR_INVALID_VALUE.
+ * ws: device workspace of fb_fft2d_workspace_bytes(n0, n1) bytes (may be NULL when that
+ * is 0 -- every n0 <= 4096).  Not read before written; contents undefined afterwards.
+ * Accuracy (north_star): rel-L2 <= 1e-5 * log2(n0 n1) vs the exact DFT; internal gate
+ * 5e-7 (reading R6). */
+size_t fb_fft2d_workspace_bytes(int64_t n0, int64_t n1);
+fb_status fb_fft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, size_t ws_bytes,
+                   void* stream);
+fb_status fb_ifft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, size_t ws_bytes,
+                    void* stream);
+
+/* ------------------------------------------------------------------ matrix block
+ * C[m][n] = A[m][k] * B[k][n]  (row-major, leading dimensions in ELEMENTS, C overwritten).
+ * FB_F64: IEEE FP64 (DMMA tensor-core FMAs, RN); accuracy rel-L2 <= 1e-12.
+ * FB_F32: FP32 via 3xTF32 on tcgen05 tensor cores (hi*hi + hi*lo + lo*hi with RN-split
+ *         operands, FP32 accumulation in TMEM); accuracy rel-L2 <= 1e-5 (reading R11).
+ *         Not bitwise equal to an FP32 SIMT GEMM.
+ * m, n, k >= 1 (any value: ragged edges are handled).  A, B, C 16-byte aligned;
+ * lda, ldb, ldc >= the row width and lda*esize, ldb*esize, ldc*esize multiples of 16 B.
+ * ws: device workspace of fb_matmul_workspace_bytes(...) bytes (FP32: the TF32 hi/lo
+ * split operands; FP64: 0).  C must not overlap A, B or ws. */
+size_t fb_matmul_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k);
+fb_status fb_matmul(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, void* C, int64_t ldc, void* ws,
+                    size_t ws_bytes, void* stream);
+
+/* The two steps of the FB_F32 path, exposed so a caller can reuse a split operand (e.g. a
+ * broadcast B) and a harness can time the tensor-core kernel alone.
+ * fb_tf32_split: X (rows x cols, ldx) -> hi, lo with hi = rna_tf32(x), lo = rna_tf32(x - hi)
+ *   (FP32 bit patterns with the low 13 mantissa bits zero).  transpose = 0 writes hi/lo as
+ *   rows x cols with leading dim ld_out (>= cols); transpose = 1 writes them as cols x rows
+ *   (ld_out >= rows).  ld_out*4 must be a multiple of 16.
+ * fb_matmul_3xtf32_presplit: C[m][n] = Ah*Bh^T + Ah*Bl^T + Al*Bh^T where Ah/Al are m x k
+ *   (ld lda) and Bh/Bl are n x k (ld ldb), i.e. both K-major, as produced by fb_tf32_split
+ *   (A with transpose = 0, B with transpose = 1).  lda*4, ldb*4, ldc*4 multiples of 16. */
+fb_status fb_tf32_split(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx,
+                        float* hi, float* lo, int64_t ld_out, void* stream);
+fb_status fb_matmul_3xtf32_presplit(int64_t m, int64_t n, int64_t k, const float* Ah,
+                                    const float* Al, int64_t lda, const float* Bh,
+                                    const float* Bl, int64_t ldb, float* C, int64_t ldc,
+                                    void* stream);
+
+/* ------------------------------------------------------------------ host interface
+ * The C-1 "connect the host program" form including the CPU<->GPU transfer the
+ * paper names as the overhead of naive offload: HOST input -> H2D -> the block ->
+ * D2H -> HOST output, all on `stream`; returns after the result is in host memory.
+ * Host buffers should be pinned (cudaHostAlloc / torch pin_memory) for full bandwidth.
+ * dev: caller-owned DEVICE scratch of *_host_workspace_bytes bytes (holds the device
+ * copies and the block's own workspace). */
+size_t fb_fft2d_host_workspace_bytes(int64_t n0, int64_t n1);
+fb_status fb_fft2d_host(const void* x_host, void* y_host, int64_t n0, int64_t n1, int inverse,
+                        void* dev, size_t dev_bytes, void* stream);
+size_t fb_matmul_host_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k);
+fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void* A_host,
+                         const void* B_host, void* C_host, void* dev, size_t dev_bytes,
+                         void* stream);
+
+/* ------------------------------------------------------------------ multi-GPU
+ * One process per GPU.  Rank 0 calls fb_comm_unique_id and the caller distributes the
+ * 128 bytes (e.g. torch.distributed broadcast); every rank then calls fb_comm_init.
+ * An fb_comm wraps an NCCL communicator bound to `device`; use it from one stream at a
+ * time. */
+typedef struct fb_comm fb_comm;
+size_t fb_comm_unique_id_bytes(void);
+fb_status fb_comm_unique_id(void* uid_out /* fb_comm_unique_id_bytes() bytes */);
+fb_status fb_comm_init(fb_comm** comm, int nranks, int rank, const void* uid, int device);
+fb_status fb_comm_destroy(fb_comm* comm);
+int fb_comm_rank(const fb_comm* comm);
+int fb_comm_size(const fb_comm* comm);
+
+/* Slab-sharded 2D FFT over P = comm size ranks (north_star (4), reading R8).
+ * Rank r owns rows [r n0/P, (r+1) n0/P) of the natural n0 x n1 array, stored as an
+ * (n0/P) x n1 row-major slab.  The forward transform returns the COLUMN slab: rank r
+ * receives all n0 rows of columns [r n1/P, (r+1) n1/P) of Y, stored row-major as an
+ * n0 x (n1/P) array.  One ncclAlltoAll (the global transpose) per call; the packing into
+ * per-peer blocks is fused into the row pass.  fb_ifft2d_slab is the exact inverse:
+ * column slab in, natural row slab out (scaled by 1/(n0 n1)).
+ * Requires n0 % P == 0 and n1 % P == 0.  x and out must not overlap.
+ * ws: fb_fft2d_slab_workspace_bytes(P, n0, n1) device bytes (send + receive buffers). */
+size_t fb_fft2d_slab_workspace_bytes(int nranks, int64_t n0, int64_t n1);
+fb_status fb_fft2d_slab(fb_comm* comm, const void* x_rows, void* y_cols, int64_t n0, int64_t n1,
+                        void* ws, size_t ws_bytes, void* stream);
+fb_status fb_ifft2d_slab(fb_comm* comm, const void* y_cols, void* x_rows, int64_t n0, int64_t n1,
+                         void* ws, size_t ws_bytes, void* stream);
+
+/* Row-block GEMM (north_star (4), reading R18): rank r owns A rows and C rows
+ * [r m/P, (r+1) m/P) as (m/P) x k and (m/P) x n row-major blocks; B (k x n) lives on
+ * `root` and is broadcast (ncclBroadcast, inside the call) into every rank's B buffer
+ * (on non-root ranks B is a receive buffer of k x n elements with leading dim ldb).
+ * Requires m % P == 0.  ws: fb_matmul_rowblock_workspace_bytes(...) device bytes. */
+size_t fb_matmul_rowblock_workspace_bytes(int nranks, int dtype, int64_t m, int64_t n, int64_t k);
+fb_status fb_matmul_rowblock(fb_comm* comm, int dtype, int64_t m, int64_t n, int64_t k,
+                             const void* A_rows, int64_t lda, void* B, int64_t ldb, int root,
+                             void* C_rows, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FB_H */

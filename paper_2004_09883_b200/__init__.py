@@ -1,0 +1,302 @@
+"""Python binding for libfb.so -- the B200-native function blocks of arXiv 2004.09883.
+
+Argument marshalling only: every step of the hot path runs in libfb's CUDA kernels
+(csrc/).  torch is used for device memory, streams and torch.distributed (plumbing).
+There is NO CPU fallback: if libfb.so is missing or the device is not sm_100, calls raise.
+
+The functions carry the C-ABI names of include/fb.h (fb_fft2d, fb_ifft2d, fb_matmul,
+fb_fft2d_host, fb_matmul_host, fb_fft2d_slab, fb_ifft2d_slab, fb_matmul_rowblock, ...);
+``fft2d``/``ifft2d``/``matmul`` are conveniences that allocate outputs/workspaces.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfb.so")
+
+FB_F32 = 0
+FB_F64 = 1
+_STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_VALUE", 2: "FB_ERR_UNSUPPORTED_SIZE", 3: "FB_ERR_MISALIGNED",
+           4: "FB_ERR_WORKSPACE", 5: "FB_ERR_NOT_INITIALIZED", 6: "FB_ERR_CUDA", 7: "FB_ERR_NCCL",
+           8: "FB_ERR_ARCH"}
+
+# every symbol include/fb.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_init",
+    "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d",
+    "fb_matmul_workspace_bytes", "fb_matmul", "fb_tf32_split", "fb_matmul_3xtf32_presplit",
+    "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
+    "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
+    "fb_comm_size", "fb_fft2d_slab_workspace_bytes", "fb_fft2d_slab", "fb_ifft2d_slab",
+    "fb_matmul_rowblock_workspace_bytes", "fb_matmul_rowblock",
+]
+
+
+class FbError(RuntimeError):
+    def __init__(self, fn, status, detail):
+        super().__init__(f"{fn}: {_STATUS.get(status, status)}: {detail}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load libfb.so (build it first with __graft_entry__.build() / _build.py)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} is missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, i64, ci, sz, u64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_size_t, ctypes.c_uint64
+    sig = {
+        "fb_version": ([], ci),
+        "fb_status_string": ([ci], ctypes.c_char_p),
+        "fb_last_error_detail": ([], ctypes.c_char_p),
+        "fb_launch_count": ([], u64),
+        "fb_init": ([ci], ci),
+        "fb_fft2d_workspace_bytes": ([i64, i64], sz),
+        "fb_fft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_ifft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_matmul_workspace_bytes": ([ci, i64, i64, i64], sz),
+        "fb_matmul": ([ci, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], ci),
+        "fb_tf32_split": ([ci, i64, i64, vp, i64, vp, vp, i64, vp], ci),
+        "fb_matmul_3xtf32_presplit": ([i64, i64, i64, vp, vp, i64, vp, vp, i64, vp, i64, vp], ci),
+        "fb_fft2d_host_workspace_bytes": ([i64, i64], sz),
+        "fb_fft2d_host": ([vp, vp, i64, i64, ci, vp, sz, vp], ci),
+        "fb_matmul_host_workspace_bytes": ([ci, i64, i64, i64], sz),
+        "fb_matmul_host": ([ci, i64, i64, i64, vp, vp, vp, vp, sz, vp], ci),
+        "fb_comm_unique_id_bytes": ([], sz),
+        "fb_comm_unique_id": ([vp], ci),
+        "fb_comm_init": ([ctypes.POINTER(vp), ci, ci, vp, ci], ci),
+        "fb_comm_destroy": ([vp], ci),
+        "fb_comm_rank": ([vp], ci),
+        "fb_comm_size": ([vp], ci),
+        "fb_fft2d_slab_workspace_bytes": ([ci, i64, i64], sz),
+        "fb_fft2d_slab": ([vp, vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_ifft2d_slab": ([vp, vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_matmul_rowblock_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
+        "fb_matmul_rowblock": ([vp, ci, i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, vp, sz, vp], ci),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def _check(fn: str, status: int):
+    if status != 0:
+        detail = lib().fb_last_error_detail().decode(errors="replace")
+        raise FbError(fn, status, detail)
+
+
+def _stream(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _ptr(t) -> int | None:
+    return None if t is None else t.data_ptr()
+
+
+def launch_count() -> int:
+    return int(lib().fb_launch_count())
+
+
+def fb_init(device: int = 0):
+    _check("fb_init", lib().fb_init(device))
+
+
+# ------------------------------------------------------------------ workspace cache (plumbing)
+_ws_cache: dict = {}
+
+
+def _workspace(nbytes: int, device) -> torch.Tensor | None:
+    if nbytes == 0:
+        return None
+    key = (torch.device(device).index, "ws")
+    t = _ws_cache.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _ws_cache[key] = t
+    return t
+
+
+# ------------------------------------------------------------------ Fourier block
+def _fft_check(x: torch.Tensor):
+    if x.dtype != torch.complex64 or not x.is_cuda or x.dim() != 2 or not x.is_contiguous():
+        raise ValueError("expected a contiguous 2D complex64 CUDA tensor")
+
+
+def fb_fft2d(x: torch.Tensor, y: torch.Tensor, ws: torch.Tensor | None = None, stream=None):
+    n0, n1 = x.shape
+    _check("fb_fft2d", lib().fb_fft2d(_ptr(x), _ptr(y), n0, n1, _ptr(ws), 0 if ws is None else ws.numel(),
+                                      _stream(stream)))
+
+
+def fb_ifft2d(x: torch.Tensor, y: torch.Tensor, ws: torch.Tensor | None = None, stream=None):
+    n0, n1 = x.shape
+    _check("fb_ifft2d", lib().fb_ifft2d(_ptr(x), _ptr(y), n0, n1, _ptr(ws), 0 if ws is None else ws.numel(),
+                                        _stream(stream)))
+
+
+def fft2d(x: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = False, stream=None) -> torch.Tensor:
+    """2D DFT (sign -1, unscaled) or inverse (sign +1, 1/(n0 n1)) of a complex64 CUDA tensor."""
+    _fft_check(x)
+    out = torch.empty_like(x) if out is None else out
+    _fft_check(out)
+    n0, n1 = x.shape
+    ws = _workspace(lib().fb_fft2d_workspace_bytes(n0, n1), x.device)
+    (fb_ifft2d if inverse else fb_fft2d)(x, out, ws, stream)
+    return out
+
+
+def ifft2d(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    return fft2d(x, out, inverse=True, stream=stream)
+
+
+# ------------------------------------------------------------------ matrix block
+def _dt(t: torch.Tensor) -> int:
+    if t.dtype == torch.float32:
+        return FB_F32
+    if t.dtype == torch.float64:
+        return FB_F64
+    raise ValueError("fb_matmul supports float32 (3xTF32) and float64 (DMMA)")
+
+
+def fb_matmul(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor, ws: torch.Tensor | None = None, stream=None):
+    m, k = A.shape
+    n = B.shape[1]
+    _check("fb_matmul", lib().fb_matmul(_dt(A), m, n, k, _ptr(A), A.stride(0), _ptr(B), B.stride(0), _ptr(C),
+                                        C.stride(0), _ptr(ws), 0 if ws is None else ws.numel(), _stream(stream)))
+
+
+def matmul_workspace_bytes(dtype: int, m: int, n: int, k: int) -> int:
+    return int(lib().fb_matmul_workspace_bytes(dtype, m, n, k))
+
+
+def matmul(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """C = A @ B for row-major float32 (3xTF32 tensor cores) or float64 (DMMA) CUDA tensors."""
+    if A.dim() != 2 or B.dim() != 2 or A.shape[1] != B.shape[0] or A.dtype != B.dtype:
+        raise ValueError("shape/dtype mismatch")
+    if A.stride(1) != 1 or B.stride(1) != 1:
+        raise ValueError("operands must be row-major with unit column stride")
+    m, k = A.shape
+    n = B.shape[1]
+    out = torch.empty((m, n), dtype=A.dtype, device=A.device) if out is None else out
+    ws = _workspace(matmul_workspace_bytes(_dt(A), m, n, k), A.device)
+    fb_matmul(A, B, out, ws, stream)
+    return out
+
+
+def fb_tf32_split(X: torch.Tensor, hi: torch.Tensor, lo: torch.Tensor, transpose: bool = False, stream=None):
+    rows, cols = X.shape
+    _check("fb_tf32_split", lib().fb_tf32_split(int(transpose), rows, cols, _ptr(X), X.stride(0), _ptr(hi), _ptr(lo),
+                                                hi.stride(0), _stream(stream)))
+
+
+def fb_matmul_3xtf32_presplit(Ah, Al, Bh, Bl, C, stream=None):
+    """C = Ah Bh^T + Ah Bl^T + Al Bh^T  (Ah/Al: m x k, Bh/Bl: n x k, all K-major)."""
+    m, k = Ah.shape
+    n = Bh.shape[0]
+    _check("fb_matmul_3xtf32_presplit", lib().fb_matmul_3xtf32_presplit(
+        m, n, k, _ptr(Ah), _ptr(Al), Ah.stride(0), _ptr(Bh), _ptr(Bl), Bh.stride(0), _ptr(C), C.stride(0),
+        _stream(stream)))
+
+
+# ------------------------------------------------------------------ host interface
+def _host_buf(n_bytes: int, device):
+    return _workspace_named(n_bytes, device, "host_dev")
+
+
+_named: dict = {}
+
+
+def _workspace_named(nbytes, device, name):
+    key = (torch.device(device).index, name)
+    t = _named.get(key)
+    if t is None or t.numel() < nbytes:
+        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        _named[key] = t
+    return t
+
+
+def fb_fft2d_host(x_host: torch.Tensor, y_host: torch.Tensor, inverse: bool = False, device=0, stream=None):
+    """HOST complex64 in -> H2D -> 2D FFT -> D2H -> HOST out (synchronous)."""
+    n0, n1 = x_host.shape
+    need = lib().fb_fft2d_host_workspace_bytes(n0, n1)
+    dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
+    _check("fb_fft2d_host", lib().fb_fft2d_host(_ptr(x_host), _ptr(y_host), n0, n1, int(inverse), _ptr(dev),
+                                                dev.numel(), _stream(stream)))
+
+
+def fb_matmul_host(A_host: torch.Tensor, B_host: torch.Tensor, C_host: torch.Tensor, device=0, stream=None):
+    m, k = A_host.shape
+    n = B_host.shape[1]
+    dt = _dt(A_host)
+    need = lib().fb_matmul_host_workspace_bytes(dt, m, n, k)
+    dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
+    _check("fb_matmul_host", lib().fb_matmul_host(dt, m, n, k, _ptr(A_host), _ptr(B_host), _ptr(C_host),
+                                                  _ptr(dev), dev.numel(), _stream(stream)))
+
+
+# ------------------------------------------------------------------ multi-GPU
+class Comm:
+    """An fb_comm (NCCL communicator) for this process's GPU.
+
+    uid distribution uses torch.distributed (any backend) -- plumbing only."""
+
+    def __init__(self, rank: int, world: int, device: int, group=None):
+        import torch.distributed as dist
+        L = lib()
+        nb = L.fb_comm_unique_id_bytes()
+        uid = torch.zeros(nb, dtype=torch.uint8)
+        if rank == 0:
+            buf = ctypes.create_string_buffer(nb)
+            _check("fb_comm_unique_id", L.fb_comm_unique_id(buf))
+            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
+        if world > 1:
+            obj = [uid.tolist()]
+            dist.broadcast_object_list(obj, src=0, group=group)
+            uid = torch.tensor(obj[0], dtype=torch.uint8)
+        raw = bytes(uid.tolist())
+        handle = ctypes.c_void_p()
+        _check("fb_comm_init", L.fb_comm_init(ctypes.byref(handle), world, rank, raw, device))
+        self.handle = handle
+        self.rank, self.world, self.device = rank, world, device
+
+    def destroy(self):
+        if self.handle:
+            _check("fb_comm_destroy", lib().fb_comm_destroy(self.handle))
+            self.handle = None
+
+    def fb_fft2d_slab(self, x_rows, y_cols, n0, n1, ws=None, stream=None):
+        need = lib().fb_fft2d_slab_workspace_bytes(self.world, n0, n1)
+        ws = _workspace_named(need, x_rows.device, "slab") if ws is None else ws
+        _check("fb_fft2d_slab", lib().fb_fft2d_slab(self.handle, _ptr(x_rows), _ptr(y_cols), n0, n1, _ptr(ws),
+                                                    ws.numel(), _stream(stream)))
+
+    def fb_ifft2d_slab(self, y_cols, x_rows, n0, n1, ws=None, stream=None):
+        need = lib().fb_fft2d_slab_workspace_bytes(self.world, n0, n1)
+        ws = _workspace_named(need, y_cols.device, "slab") if ws is None else ws
+        _check("fb_ifft2d_slab", lib().fb_ifft2d_slab(self.handle, _ptr(y_cols), _ptr(x_rows), n0, n1, _ptr(ws),
+                                                      ws.numel(), _stream(stream)))
+
+    def fb_matmul_rowblock(self, A_rows, B, C_rows, root=0, ws=None, stream=None):
+        mp, k = A_rows.shape
+        n = B.shape[1]
+        m = mp * self.world
+        dt = _dt(A_rows)
+        need = lib().fb_matmul_rowblock_workspace_bytes(self.world, dt, m, n, k)
+        ws = _workspace_named(need, A_rows.device, "rowblock") if ws is None else ws
+        _check("fb_matmul_rowblock", lib().fb_matmul_rowblock(
+            self.handle, dt, m, n, k, _ptr(A_rows), A_rows.stride(0), _ptr(B), B.stride(0), root, _ptr(C_rows),
+            C_rows.stride(0), _ptr(ws), ws.numel(), _stream(stream)))

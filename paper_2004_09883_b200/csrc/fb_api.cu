@@ -1,0 +1,376 @@
+// fb_api.cu -- the C ABI of libfb.so (include/fb.h): validation, per-device state, entry points.
+#include <stdarg.h>
+#include <string.h>
+
+#include <mutex>
+
+#include "fb_common.cuh"
+
+namespace fb {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local char t_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(t_err, sizeof(t_err), fmt, ap);
+    va_end(ap);
+}
+void clear_error() { t_err[0] = 0; }
+
+static constexpr int kMaxDev = 64;
+static DeviceState g_dev[kMaxDev];
+static std::mutex g_dev_mu;
+
+// W[j] = exp(-2 pi i j / 16384): FP64 sincospi of the exact rational 2j/16384, RN to FP32.
+// sincospi is exact at multiples of 1/2, so +-1 and 0 are exact.
+__global__ void build_twiddles_kernel(float2* w) {
+    int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < kTwN) {
+        double s, c;
+        sincospi((double)(2 * j) / (double)kTwN, &s, &c);
+        w[j] = make_float2((float)c, (float)(-s));
+    }
+}
+
+// Stage tables: entry e = master[idx[e]] (same FP32 values as the master table).
+__global__ void gather_twiddles_kernel(const float2* __restrict__ w, const int32_t* __restrict__ idx,
+                                       float2* __restrict__ out, int64_t n) {
+    int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < n) out[e] = w[idx[e]];
+}
+
+static fb_status init_device_locked(int dev) {
+    DeviceState& st = g_dev[dev];
+    if (st.ready) return FB_OK;
+    cudaDeviceProp prop;
+    FB_CUDA_TRY(cudaGetDeviceProperties(&prop, dev));
+    if (prop.major != 10 || prop.minor != 0) {
+        set_error("device %d is sm_%d%d; libfb is built for sm_100a only", dev, prop.major, prop.minor);
+        return FB_ERR_ARCH;
+    }
+    int cur = 0;
+    FB_CUDA_TRY(cudaGetDevice(&cur));
+    FB_CUDA_TRY(cudaSetDevice(dev));
+    fb_status rc = FB_OK;
+    float2* tw = nullptr;
+    float2* stw = nullptr;
+    int32_t* didx = nullptr;
+    const int64_t nst = stage_tw_total();
+    int32_t* hidx = new int32_t[nst];
+    stage_tw_index(hidx);
+    cudaError_t e = cudaMalloc(&tw, sizeof(float2) * kTwN);
+    if (e == cudaSuccess) e = cudaMalloc(&stw, sizeof(float2) * nst);
+    if (e == cudaSuccess) e = cudaMalloc(&didx, sizeof(int32_t) * nst);
+    if (e == cudaSuccess) e = cudaMemcpy(didx, hidx, sizeof(int32_t) * nst, cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) {
+        build_twiddles_kernel<<<kTwN / 256, 256>>>(tw);
+        gather_twiddles_kernel<<<(unsigned)((nst + 255) / 256), 256>>>(tw, didx, stw, nst);
+        e = cudaGetLastError();
+        if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    }
+    delete[] hidx;
+    if (didx) cudaFree(didx);
+    if (e != cudaSuccess) {
+        set_error("fb_init(%d): %s", dev, cudaGetErrorString(e));
+        rc = FB_ERR_CUDA;
+    } else {
+        st.twiddles = tw;
+        st.stage_tw = stw;
+        st.sm_count = prop.multiProcessorCount;
+        st.ready = true;
+    }
+    cudaSetDevice(cur);
+    return rc;
+}
+
+fb_status ensure_device(int* dev_out, DeviceState** st_out) {
+    int dev = 0;
+    FB_CUDA_TRY(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= kMaxDev) {
+        set_error("device ordinal %d out of range", dev);
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!g_dev[dev].ready) {
+        std::lock_guard<std::mutex> lk(g_dev_mu);
+        FB_TRY(init_device_locked(dev));
+    }
+    if (dev_out) *dev_out = dev;
+    *st_out = &g_dev[dev];
+    return FB_OK;
+}
+
+static fb_status check_fft_dims(int64_t n0, int64_t n1) {
+    if (n0 <= 0 || n1 <= 0) {
+        set_error("n0=%lld n1=%lld must be >= 1", (long long)n0, (long long)n1);
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!is_pow2(n0) || !is_pow2(n1) || n0 > kTwN || n1 > kTwN) {
+        set_error("FFT sizes must be powers of two in [1, %d] (got %lld x %lld)", kTwN,
+                  (long long)n0, (long long)n1);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    return FB_OK;
+}
+
+static fb_status fft_entry(const void* x, void* y, int64_t n0, int64_t n1, void* ws,
+                           size_t ws_bytes, void* stream, bool inverse) {
+    clear_error();
+    FB_TRY(check_fft_dims(n0, n1));
+    if (!x || !y) {
+        set_error("null x or y");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!aligned16(x) || !aligned16(y)) {
+        set_error("x and y must be 16-byte aligned");
+        return FB_ERR_MISALIGNED;
+    }
+    const size_t bytes = (size_t)n0 * (size_t)n1 * sizeof(float2);
+    if (ranges_partially_overlap(x, bytes, y, bytes)) {
+        set_error("x and y partially overlap (exact aliasing is allowed)");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const size_t need = fft2d_ws_bytes(n0, n1);
+    if (need && (!ws || ws_bytes < need)) {
+        set_error("workspace of %zu bytes required, got %zu", need, ws_bytes);
+        return FB_ERR_WORKSPACE;
+    }
+    if (need && (ranges_overlap(ws, need, x, bytes) || ranges_overlap(ws, need, y, bytes))) {
+        set_error("workspace overlaps x or y");
+        return FB_ERR_INVALID_VALUE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    return fft2d_device(x, y, n0, n1, inverse, ws, ws_bytes, st, (cudaStream_t)stream);
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+int fb_version(void) { return 100; }
+
+const char* fb_status_string(int s) {
+    switch (s) {
+        case FB_OK: return "FB_OK";
+        case FB_ERR_INVALID_VALUE: return "FB_ERR_INVALID_VALUE";
+        case FB_ERR_UNSUPPORTED_SIZE: return "FB_ERR_UNSUPPORTED_SIZE";
+        case FB_ERR_MISALIGNED: return "FB_ERR_MISALIGNED";
+        case FB_ERR_WORKSPACE: return "FB_ERR_WORKSPACE";
+        case FB_ERR_NOT_INITIALIZED: return "FB_ERR_NOT_INITIALIZED";
+        case FB_ERR_CUDA: return "FB_ERR_CUDA";
+        case FB_ERR_NCCL: return "FB_ERR_NCCL";
+        case FB_ERR_ARCH: return "FB_ERR_ARCH";
+    }
+    return "FB_ERR_UNKNOWN";
+}
+
+const char* fb_last_error_detail(void) { return t_err; }
+
+uint64_t fb_launch_count(void) { return g_launches.load(); }
+
+fb_status fb_init(int device) {
+    clear_error();
+    if (device < 0 || device >= kMaxDev) {
+        set_error("device ordinal %d out of range", device);
+        return FB_ERR_INVALID_VALUE;
+    }
+    int n = 0;
+    FB_CUDA_TRY(cudaGetDeviceCount(&n));
+    if (device >= n) {
+        set_error("device %d does not exist (%d devices)", device, n);
+        return FB_ERR_INVALID_VALUE;
+    }
+    std::lock_guard<std::mutex> lk(g_dev_mu);
+    return init_device_locked(device);
+}
+
+size_t fb_fft2d_workspace_bytes(int64_t n0, int64_t n1) {
+    if (check_fft_dims(n0, n1) != FB_OK) return 0;
+    return fft2d_ws_bytes(n0, n1);
+}
+
+fb_status fb_fft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, size_t ws_bytes,
+                   void* stream) {
+    return fft_entry(x, y, n0, n1, ws, ws_bytes, stream, false);
+}
+
+fb_status fb_ifft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, size_t ws_bytes,
+                    void* stream) {
+    return fft_entry(x, y, n0, n1, ws, ws_bytes, stream, true);
+}
+
+size_t fb_matmul_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
+    if ((dtype != FB_F32 && dtype != FB_F64) || m <= 0 || n <= 0 || k <= 0) return 0;
+    return gemm_ws_bytes(dtype, m, n, k);
+}
+
+fb_status fb_matmul(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
+                    void* stream) {
+    clear_error();
+    if (dtype != FB_F32 && dtype != FB_F64) {
+        set_error("dtype must be FB_F32 or FB_F64");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (m <= 0 || n <= 0 || k <= 0) {
+        set_error("m, n, k must be >= 1");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!A || !B || !C) {
+        set_error("null operand");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (lda < k || ldb < n || ldc < n) {
+        set_error("leading dimensions too small");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const int64_t es = dtype == FB_F32 ? 4 : 8;
+    if (!aligned16(A) || !aligned16(B) || !aligned16(C) || (lda * es) % 16 || (ldb * es) % 16 ||
+        (ldc * es) % 16) {
+        set_error("operands must be 16-byte aligned and ld*elemsize a multiple of 16");
+        return FB_ERR_MISALIGNED;
+    }
+    const size_t cbytes = (size_t)((m - 1) * ldc + n) * es;
+    if (ranges_overlap(C, cbytes, A, (size_t)((m - 1) * lda + k) * es) ||
+        ranges_overlap(C, cbytes, B, (size_t)((k - 1) * ldb + n) * es)) {
+        set_error("C overlaps A or B");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const size_t need = gemm_ws_bytes(dtype, m, n, k);
+    if (need && (!ws || ws_bytes < need || !aligned16(ws))) {
+        set_error("workspace of %zu bytes (16B aligned) required, got %zu", need, ws_bytes);
+        return FB_ERR_WORKSPACE;
+    }
+    if (need && ranges_overlap(ws, need, C, cbytes)) {
+        set_error("workspace overlaps C");
+        return FB_ERR_INVALID_VALUE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    return gemm_device(dtype, m, n, k, A, lda, B, ldb, C, ldc, ws, ws_bytes, st,
+                       (cudaStream_t)stream);
+}
+
+fb_status fb_tf32_split(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
+                        float* lo, int64_t ld_out, void* stream) {
+    clear_error();
+    if (rows <= 0 || cols <= 0 || !X || !hi || !lo || (transpose != 0 && transpose != 1) || ldx < cols ||
+        ld_out < (transpose ? rows : cols)) {
+        set_error("bad fb_tf32_split arguments");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!aligned16(hi) || !aligned16(lo) || (ld_out * 4) % 16) {
+        set_error("hi/lo must be 16-byte aligned with ld_out*4 a multiple of 16");
+        return FB_ERR_MISALIGNED;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    return tf32_split_device(transpose, rows, cols, X, ldx, hi, lo, ld_out, st, (cudaStream_t)stream);
+}
+
+fb_status fb_matmul_3xtf32_presplit(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
+                                    int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
+                                    int64_t ldc, void* stream) {
+    clear_error();
+    if (m <= 0 || n <= 0 || k <= 0 || !Ah || !Al || !Bh || !Bl || !C || lda < k || ldb < k || ldc < n) {
+        set_error("bad fb_matmul_3xtf32_presplit arguments");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) {
+        set_error("dimension exceeds int32");
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    if (!aligned16(Ah) || !aligned16(Al) || !aligned16(Bh) || !aligned16(Bl) || !aligned16(C) || (lda * 4) % 16 ||
+        (ldb * 4) % 16 || (ldc * 4) % 16) {
+        set_error("operands must be 16-byte aligned, ld*4 multiples of 16");
+        return FB_ERR_MISALIGNED;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    return gemm_3xtf32_presplit_device(m, n, k, Ah, Al, lda, Bh, Bl, ldb, C, ldc, (cudaStream_t)stream);
+}
+
+// ---------------------------------------------------------------- host interface
+static size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+size_t fb_fft2d_host_workspace_bytes(int64_t n0, int64_t n1) {
+    if (check_fft_dims(n0, n1) != FB_OK) return 0;
+    return round_up((size_t)n0 * n1 * sizeof(float2), 256) + fft2d_ws_bytes(n0, n1);
+}
+
+fb_status fb_fft2d_host(const void* x_host, void* y_host, int64_t n0, int64_t n1, int inverse,
+                        void* dev, size_t dev_bytes, void* stream) {
+    clear_error();
+    FB_TRY(check_fft_dims(n0, n1));
+    if (!x_host || !y_host || !dev) {
+        set_error("null pointer");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const size_t need = fb_fft2d_host_workspace_bytes(n0, n1);
+    if (dev_bytes < need || !aligned16(dev)) {
+        set_error("device scratch of %zu bytes (16B aligned) required, got %zu", need, dev_bytes);
+        return FB_ERR_WORKSPACE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)n0 * n1 * sizeof(float2);
+    char* d = (char*)dev;
+    void* ws = d + round_up(bytes, 256);
+    FB_CUDA_TRY(cudaMemcpyAsync(d, x_host, bytes, cudaMemcpyHostToDevice, s));
+    FB_TRY(fft2d_device(d, d, n0, n1, inverse != 0, ws, fft2d_ws_bytes(n0, n1), st, s));
+    FB_CUDA_TRY(cudaMemcpyAsync(y_host, d, bytes, cudaMemcpyDeviceToHost, s));
+    FB_CUDA_TRY(cudaStreamSynchronize(s));
+    return FB_OK;
+}
+
+size_t fb_matmul_host_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
+    if ((dtype != FB_F32 && dtype != FB_F64) || m <= 0 || n <= 0 || k <= 0) return 0;
+    const size_t es = dtype == FB_F32 ? 4 : 8;
+    return round_up(m * k * es, 256) + round_up(k * n * es, 256) + round_up(m * n * es, 256) +
+           gemm_ws_bytes(dtype, m, n, k);
+}
+
+fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void* A_host,
+                         const void* B_host, void* C_host, void* dev, size_t dev_bytes,
+                         void* stream) {
+    clear_error();
+    if ((dtype != FB_F32 && dtype != FB_F64) || m <= 0 || n <= 0 || k <= 0) {
+        set_error("bad dtype or size");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!A_host || !B_host || !C_host || !dev) {
+        set_error("null pointer");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const size_t es = dtype == FB_F32 ? 4 : 8;
+    if ((k * es) % 16 || (n * es) % 16) {
+        set_error("host variant packs rows densely: k*esize and n*esize must be multiples of 16");
+        return FB_ERR_MISALIGNED;
+    }
+    const size_t need = fb_matmul_host_workspace_bytes(dtype, m, n, k);
+    if (dev_bytes < need || !aligned16(dev)) {
+        set_error("device scratch of %zu bytes required, got %zu", need, dev_bytes);
+        return FB_ERR_WORKSPACE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    cudaStream_t s = (cudaStream_t)stream;
+    char* d = (char*)dev;
+    char* dA = d;
+    char* dB = dA + round_up(m * k * es, 256);
+    char* dC = dB + round_up(k * n * es, 256);
+    char* ws = dC + round_up(m * n * es, 256);
+    FB_CUDA_TRY(cudaMemcpyAsync(dA, A_host, m * k * es, cudaMemcpyHostToDevice, s));
+    FB_CUDA_TRY(cudaMemcpyAsync(dB, B_host, k * n * es, cudaMemcpyHostToDevice, s));
+    FB_TRY(gemm_device(dtype, m, n, k, dA, k, dB, n, dC, n, ws, gemm_ws_bytes(dtype, m, n, k), st, s));
+    FB_CUDA_TRY(cudaMemcpyAsync(C_host, dC, m * n * es, cudaMemcpyDeviceToHost, s));
+    FB_CUDA_TRY(cudaStreamSynchronize(s));
+    return FB_OK;
+}
+
+}  // extern "C"

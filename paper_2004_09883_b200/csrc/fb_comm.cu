@@ -1,0 +1,241 @@
+// fb_comm.cu -- multi-GPU partitioning of the two blocks over one NVLink/NVSwitch box
+// (north_star (4)): the slab-sharded 2D FFT whose global transpose is one NCCL all-to-all,
+// and the row-block GEMM with B broadcast.  One process per GPU; NCCL communicator from a
+// unique id the caller distributes (torch.distributed in the Python binding).
+#include <nccl.h>
+#include <string.h>
+
+#include "fb_common.cuh"
+
+struct fb_comm {
+    ncclComm_t nccl = nullptr;
+    int rank = 0, size = 1, device = 0;
+};
+
+namespace fb {
+
+#define FB_NCCL_TRY(expr, comm)                                                                 \
+    do {                                                                                        \
+        ncclResult_t _r = (expr);                                                               \
+        if (_r != ncclSuccess) {                                                                \
+            ::fb::set_error("%s failed: %s (%s)", #expr, ncclGetErrorString(_r),                \
+                            (comm) ? ncclGetLastError(comm) : "");                              \
+            return FB_ERR_NCCL;                                                                 \
+        }                                                                                       \
+    } while (0)
+
+static LineMap lmap(int64_t hi, int64_t lo, int64_t es, int kb_shift = 30, int64_t bs = 0) {
+    LineMap m;
+    m.hi = hi;
+    m.lo = lo;
+    m.es = es;
+    m.kb_shift = kb_shift;
+    m.bs = bs;
+    return m;
+}
+
+static fb_status check_slab(fb_comm* c, const void* a, const void* b, int64_t n0, int64_t n1,
+                            void* ws, size_t ws_bytes) {
+    if (!c || !c->nccl) {
+        set_error("communicator is null or destroyed");
+        return FB_ERR_NOT_INITIALIZED;
+    }
+    if (n0 <= 0 || n1 <= 0) {
+        set_error("n0, n1 must be >= 1");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!is_pow2(n0) || !is_pow2(n1) || n0 > kTwN || n1 > kTwN) {
+        set_error("FFT sizes must be powers of two in [1, %d]", kTwN);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    if (n0 % c->size || n1 % c->size) {
+        set_error("n0 and n1 must be divisible by the world size %d", c->size);
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!a || !b) {
+        set_error("null input or output");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!aligned16(a) || !aligned16(b) || !aligned16(ws)) {
+        set_error("buffers must be 16-byte aligned");
+        return FB_ERR_MISALIGNED;
+    }
+    const size_t slab = (size_t)(n0 / c->size) * n1 * sizeof(float2);
+    if (ranges_overlap(a, slab, b, slab)) {
+        set_error("input and output slabs must not overlap");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!ws || ws_bytes < 2 * slab) {
+        set_error("slab workspace of %zu bytes required, got %zu", 2 * slab, ws_bytes);
+        return FB_ERR_WORKSPACE;
+    }
+    if (ranges_overlap(ws, 2 * slab, a, slab) || ranges_overlap(ws, 2 * slab, b, slab)) {
+        set_error("workspace overlaps input or output");
+        return FB_ERR_INVALID_VALUE;
+    }
+    return FB_OK;
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+size_t fb_comm_unique_id_bytes(void) { return NCCL_UNIQUE_ID_BYTES; }
+
+fb_status fb_comm_unique_id(void* uid_out) {
+    clear_error();
+    if (!uid_out) {
+        set_error("null uid buffer");
+        return FB_ERR_INVALID_VALUE;
+    }
+    ncclUniqueId id;
+    FB_NCCL_TRY(ncclGetUniqueId(&id), (ncclComm_t) nullptr);
+    memcpy(uid_out, &id, sizeof(id));
+    return FB_OK;
+}
+
+fb_status fb_comm_init(fb_comm** comm, int nranks, int rank, const void* uid, int device) {
+    clear_error();
+    if (!comm || !uid || nranks < 1 || rank < 0 || rank >= nranks) {
+        set_error("bad fb_comm_init arguments");
+        return FB_ERR_INVALID_VALUE;
+    }
+    FB_TRY(fb_init(device));
+    FB_CUDA_TRY(cudaSetDevice(device));
+    ncclUniqueId id;
+    memcpy(&id, uid, sizeof(id));
+    fb_comm* c = new fb_comm();
+    c->rank = rank;
+    c->size = nranks;
+    c->device = device;
+    ncclResult_t r = ncclCommInitRank(&c->nccl, nranks, id, rank);
+    if (r != ncclSuccess) {
+        set_error("ncclCommInitRank failed: %s", ncclGetErrorString(r));
+        delete c;
+        return FB_ERR_NCCL;
+    }
+    *comm = c;
+    return FB_OK;
+}
+
+fb_status fb_comm_destroy(fb_comm* c) {
+    clear_error();
+    if (!c) return FB_OK;
+    fb_status st = FB_OK;
+    if (c->nccl) {
+        ncclResult_t r = ncclCommDestroy(c->nccl);
+        if (r != ncclSuccess) {
+            set_error("ncclCommDestroy failed: %s", ncclGetErrorString(r));
+            st = FB_ERR_NCCL;
+        }
+        c->nccl = nullptr;
+    }
+    delete c;
+    return st;
+}
+
+int fb_comm_rank(const fb_comm* c) { return c ? c->rank : -1; }
+int fb_comm_size(const fb_comm* c) { return c ? c->size : -1; }
+
+size_t fb_fft2d_slab_workspace_bytes(int nranks, int64_t n0, int64_t n1) {
+    if (nranks < 1 || n0 <= 0 || n1 <= 0 || n0 % nranks) return 0;
+    return 2 * (size_t)(n0 / nranks) * (size_t)n1 * sizeof(float2);
+}
+
+// Forward: natural row slab (n0/P x n1) -> column slab (n0 x n1/P).
+//   1. row FFTs, the store scatters element k of local row i into the per-peer send block
+//      d = k / (n1/P) at [i][k mod (n1/P)]  (pack fused into the row pass)
+//   2. ncclAlltoAll: block from rank s lands at recv[s] = rows [s n0/P, (s+1) n0/P) of the
+//      column strip -> recv IS the natural n0 x (n1/P) strip
+//   3. column FFTs of length n0 on the strip (four-step if n0 > 4096)
+fb_status fb_fft2d_slab(fb_comm* c, const void* x_rows, void* y_cols, int64_t n0, int64_t n1, void* ws,
+                        size_t ws_bytes, void* stream) {
+    clear_error();
+    FB_TRY(check_slab(c, x_rows, y_cols, n0, n1, ws, ws_bytes));
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int P = c->size;
+    const int64_t rows = n0 / P, cols = n1 / P;
+    const size_t slab = (size_t)rows * n1;
+    float2* send = (float2*)ws;
+    float2* recv = send + slab;
+
+    FftPass p{};
+    p.in = (const float2*)x_rows;
+    p.out = send;
+    p.log2L = ilog2(n1);
+    p.nlines = rows;
+    p.g_shift = 0;
+    p.lin = lmap(n1, 0, 1);
+    p.lout = lmap(cols, 0, 1, ilog2(cols), rows * cols);
+    p.scale = 1.f;
+    p.col_like = 0;
+    FB_TRY(launch_fft_pass(p, st, s));
+    FB_NCCL_TRY(ncclAlltoAll(send, recv, (size_t)rows * cols * 2, ncclFloat, c->nccl, s), c->nccl);
+    return fft_columns(recv, (float2*)y_cols, n0, cols, cols, cols, false, false, 1.f, recv, st, s);
+}
+
+// Inverse: column slab (n0 x n1/P) -> natural row slab (n0/P x n1), scaled by 1/(n0 n1).
+fb_status fb_ifft2d_slab(fb_comm* c, const void* y_cols, void* x_rows, int64_t n0, int64_t n1, void* ws,
+                         size_t ws_bytes, void* stream) {
+    clear_error();
+    FB_TRY(check_slab(c, y_cols, x_rows, n0, n1, ws, ws_bytes));
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    cudaStream_t s = (cudaStream_t)stream;
+    const int P = c->size;
+    const int64_t rows = n0 / P, cols = n1 / P;
+    const size_t slab = (size_t)rows * n1;
+    float2* send = (float2*)ws;
+    float2* recv = send + slab;
+    // 1. column IFFTs (conj in), natural strip into `send`: rows of peer d are contiguous
+    FB_TRY(fft_columns((const float2*)y_cols, send, n0, cols, cols, cols, true, false, 1.f, recv, st, s));
+    // 2. global transpose back
+    FB_NCCL_TRY(ncclAlltoAll(send, recv, (size_t)rows * cols * 2, ncclFloat, c->nccl, s), c->nccl);
+    // 3. row IFFTs; the load gathers element k of local row i from recv[k/(n1/P)][i][k mod (n1/P)]
+    FftPass p{};
+    p.in = recv;
+    p.out = (float2*)x_rows;
+    p.log2L = ilog2(n1);
+    p.nlines = rows;
+    p.g_shift = 0;
+    p.lin = lmap(cols, 0, 1, ilog2(cols), rows * cols);
+    p.lout = lmap(n1, 0, 1);
+    p.conj_out = 1;
+    p.scale = 1.0f / (float)((double)n0 * (double)n1);
+    p.col_like = 0;
+    return launch_fft_pass(p, st, s);
+}
+
+size_t fb_matmul_rowblock_workspace_bytes(int nranks, int dtype, int64_t m, int64_t n, int64_t k) {
+    if (nranks < 1 || m <= 0 || n <= 0 || k <= 0 || m % nranks) return 0;
+    if (dtype != FB_F32 && dtype != FB_F64) return 0;
+    return gemm_ws_bytes(dtype, m / nranks, n, k);
+}
+
+fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_t k, const void* A_rows,
+                             int64_t lda, void* B, int64_t ldb, int root, void* C_rows, int64_t ldc,
+                             void* ws, size_t ws_bytes, void* stream) {
+    clear_error();
+    if (!c || !c->nccl) {
+        set_error("communicator is null or destroyed");
+        return FB_ERR_NOT_INITIALIZED;
+    }
+    if (m <= 0 || n <= 0 || k <= 0 || m % c->size || root < 0 || root >= c->size) {
+        set_error("bad sizes (m %% P must be 0) or root");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!B || ldb != n) {
+        set_error("B must be a dense k x n buffer (ldb == n) on every rank");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const ncclDataType_t t = dtype == FB_F64 ? ncclDouble : ncclFloat;
+    // B broadcast from root (in place on root) -- the only data exchange of the row-block GEMM
+    FB_NCCL_TRY(ncclBroadcast(B, B, (size_t)k * (size_t)n, t, root, c->nccl, (cudaStream_t)stream), c->nccl);
+    return fb_matmul(dtype, m / c->size, n, k, A_rows, lda, B, ldb, C_rows, ldc, ws, ws_bytes, stream);
+}
+
+}  // extern "C"

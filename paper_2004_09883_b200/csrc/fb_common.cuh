@@ -1,0 +1,128 @@
+// fb_common.cuh -- shared host/device plumbing for libfb (sm_100a only).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/fb.h"
+
+#if defined(__CUDA_ARCH__) && (__CUDA_ARCH__ != 1000)
+#error "libfb kernels are written for sm_100a only (compile with -gencode arch=compute_100a,code=sm_100a)"
+#endif
+
+namespace fb {
+
+// ---------------------------------------------------------------- error reporting
+void set_error(const char* fmt, ...);
+void clear_error();
+extern std::atomic<uint64_t> g_launches;
+
+#define FB_CUDA_TRY(expr)                                                                  \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess) {                                                           \
+            ::fb::set_error("%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                            __LINE__);                                                     \
+            return FB_ERR_CUDA;                                                            \
+        }                                                                                  \
+    } while (0)
+
+// Check the launch that was just enqueued and count it.
+#define FB_LAUNCH_CHECK(name)                                                              \
+    do {                                                                                   \
+        cudaError_t _e = cudaGetLastError();                                               \
+        if (_e != cudaSuccess) {                                                           \
+            ::fb::set_error("launch of %s failed: %s", name, cudaGetErrorString(_e));       \
+            return FB_ERR_CUDA;                                                            \
+        }                                                                                  \
+        ::fb::g_launches.fetch_add(1, std::memory_order_relaxed);                          \
+    } while (0)
+
+#define FB_TRY(expr)                      \
+    do {                                  \
+        fb_status _s = (expr);            \
+        if (_s != FB_OK) return _s;       \
+    } while (0)
+
+// Per-device immutable state (twiddle table pointer, SM count, ...).
+struct DeviceState {
+    bool ready = false;
+    int sm_count = 0;
+    float2* twiddles = nullptr;  // 16384 entries, W[j] = exp(-2 pi i j / 16384)
+    float2* stage_tw = nullptr;  // per-(line length, stage) contiguous twiddles (fb_fft.cu)
+};
+int64_t stage_tw_total();
+void stage_tw_index(int32_t* idx);
+fb_status ensure_device(int* dev_out, DeviceState** st_out);
+
+constexpr int kTwLog2 = 14;
+constexpr int kTwN = 1 << kTwLog2;  // twiddle table resolution (max line length)
+
+inline bool is_pow2(int64_t n) { return n > 0 && (n & (n - 1)) == 0; }
+inline int ilog2(int64_t n) {
+    int l = 0;
+    while ((int64_t(1) << l) < n) ++l;
+    return l;
+}
+inline bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+inline bool ranges_partially_overlap(const void* a, size_t na, const void* b, size_t nb) {
+    uintptr_t a0 = (uintptr_t)a, a1 = a0 + na, b0 = (uintptr_t)b, b1 = b0 + nb;
+    bool overlap = a0 < b1 && b0 < a1;
+    return overlap && !(a0 == b0 && na == nb);
+}
+inline bool ranges_overlap(const void* a, size_t na, const void* b, size_t nb) {
+    uintptr_t a0 = (uintptr_t)a, a1 = a0 + na, b0 = (uintptr_t)b, b1 = b0 + nb;
+    return na && nb && a0 < b1 && b0 < a1;
+}
+
+// ---------------------------------------------------------------- FFT internals
+// One "pass" = length-L FFTs along a set of lines (see fb_fft.cu for the addressing).
+struct LineMap {
+    // line g -> base = (g >> g_shift) * hi + (g & ((1<<g_shift)-1)) * lo
+    int64_t hi, lo;
+    // element k -> (k & ((1<<kb_shift)-1)) * es + (k >> kb_shift) * bs
+    int kb_shift;
+    int64_t es, bs;
+};
+struct FftPass {
+    const float2* in;
+    float2* out;
+    int log2L;
+    int64_t nlines;
+    int g_shift;
+    LineMap lin, lout;
+    int conj_in, conj_out;
+    float scale;
+    int tw4_log2N;  // >0: four-step twiddle W_N^{(g >> g_shift) * k} on the output, N = 2^tw4_log2N
+    int col_like;   // 1: adjacent lines are adjacent in memory (pick a wide C for coalescing)
+};
+fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t s);
+
+// Full single-GPU 2D FFT on device buffers (used by the API and the host/slab variants).
+size_t fft2d_ws_bytes(int64_t n0, int64_t n1);
+fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
+                       size_t ws_bytes, const DeviceState* st, cudaStream_t s);
+// Column transform of an n0 x ncols block with leading dimension ld (in place allowed when
+// n0 <= 4096); used by 2D and slab paths.
+fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, int64_t ld_in,
+                      int64_t ld_out, bool conj_in, bool conj_out, float scale, float2* tmp,
+                      const DeviceState* st, cudaStream_t s);
+
+// ---------------------------------------------------------------- GEMM internals
+size_t gemm_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k);
+fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                      const void* B, int64_t ldb, void* C, int64_t ldc, void* ws,
+                      size_t ws_bytes, const DeviceState* st, cudaStream_t s);
+
+// G1: TF32 split (transpose=0: X[rows][cols] -> hi/lo [rows][ldo]; transpose=1: -> [cols][ldo])
+fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
+                            float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s);
+// G2-G4: C = Ah*Bh^T + Ah*Bl^T + Al*Bh^T with K-major split operands (A: m x k, B^T: n x k)
+fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
+                                      int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
+                                      int64_t ldc, cudaStream_t s);
+
+}  // namespace fb

@@ -1,0 +1,80 @@
+"""C-ABI boundary checks that need no GPU: libfb.so loads, exports every symbol include/fb.h
+declares, and rejects invalid arguments synchronously (before touching the device)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _header_symbols():
+    src = open(os.path.join(ROOT, "include", "fb.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(fb_[a-z0-9_]+)\s*\(", src)))
+
+
+@pytest.fixture(scope="module")
+def L():
+    import __graft_entry__
+    __graft_entry__.build_lib()
+    import paper_2004_09883_b200 as fb
+    return fb.lib()
+
+
+def test_exports_every_declared_symbol(L):
+    import paper_2004_09883_b200 as fb
+    syms = _header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(fb.EXPORTS) == syms
+
+
+def test_status_strings_and_version(L):
+    assert L.fb_version() >= 100
+    assert L.fb_status_string(0) == b"FB_OK"
+    assert L.fb_status_string(2) == b"FB_ERR_UNSUPPORTED_SIZE"
+    assert L.fb_status_string(99) == b"FB_ERR_UNKNOWN"
+
+
+def test_fft_validation_without_device(L):
+    p = ctypes.c_void_p(16)
+    # not a power of two -> FB_ERR_UNSUPPORTED_SIZE (2), nothing enqueued
+    assert L.fb_fft2d(p, p, 3, 4, None, 0, None) == 2
+    assert L.fb_fft2d(p, p, 32768, 4, None, 0, None) == 2
+    assert b"power" in L.fb_last_error_detail()
+    assert L.fb_fft2d(p, p, 0, 4, None, 0, None) == 1
+    assert L.fb_fft2d(None, p, 4, 4, None, 0, None) == 1
+    # misaligned
+    assert L.fb_fft2d(ctypes.c_void_p(8), p, 4, 4, None, 0, None) == 3
+    # partial overlap: x = 16, y = 24 (sizes 128 bytes)
+    assert L.fb_ifft2d(ctypes.c_void_p(16), ctypes.c_void_p(32), 4, 4, None, 0, None) == 1
+    # workspace rules
+    assert L.fb_fft2d_workspace_bytes(2048, 2048) == 0
+    assert L.fb_fft2d_workspace_bytes(8192, 64) == 8192 * 64 * 8
+    assert L.fb_fft2d(p, ctypes.c_void_p(1 << 40), 8192, 64, None, 0, None) == 4
+
+
+def test_matmul_validation_without_device(L):
+    p = ctypes.c_void_p(1 << 20)
+    q = ctypes.c_void_p(1 << 30)
+    r = ctypes.c_void_p(1 << 35)
+    assert L.fb_matmul(2, 4, 4, 4, p, 4, q, 4, r, 4, None, 0, None) == 1        # bad dtype
+    assert L.fb_matmul(1, 0, 4, 4, p, 4, q, 4, r, 4, None, 0, None) == 1        # m = 0
+    assert L.fb_matmul(1, 4, 4, 4, p, 3, q, 4, r, 4, None, 0, None) == 1        # lda < k
+    assert L.fb_matmul(0, 4, 4, 5, p, 5, q, 4, r, 4, None, 0, None) == 3        # lda*4 % 16
+    assert L.fb_matmul(1, 4, 4, 4, p, 4, p, 4, p, 4, None, 0, None) == 1        # C aliases A
+    assert L.fb_matmul(0, 64, 64, 64, p, 64, q, 64, r, 64, None, 0, None) == 4  # FP32 needs ws
+    assert L.fb_matmul_workspace_bytes(1, 64, 64, 64) == 0
+    assert L.fb_matmul_workspace_bytes(0, 64, 32, 30) == (2 * 64 * 32 + 2 * 32 * 32) * 4
+
+
+def test_comm_validation_without_device(L):
+    assert L.fb_comm_unique_id_bytes() == 128
+    p = ctypes.c_void_p(16)
+    assert L.fb_fft2d_slab(None, p, p, 16, 16, p, 4096, None) == 5
+    assert L.fb_matmul_rowblock(None, 0, 8, 8, 8, p, 8, p, 8, 0, p, 8, None, 0, None) == 5
+    assert L.fb_comm_destroy(None) == 0
+    assert L.fb_fft2d_slab_workspace_bytes(4, 64, 32) == 2 * 16 * 32 * 8

@@ -1,0 +1,167 @@
+"""GPU parity of the Fourier block (fb_fft2d / fb_ifft2d through the C ABI) against the oracle.
+
+Bars (north_star): rel-L2 <= 1e-5 * log2(n0 n1); internal gate 5e-7 on uniform inputs
+(reading R6) for sizes where the full oracle runs.
+"""
+import itertools
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def fb():
+    import __graft_entry__
+    __graft_entry__.build_lib()
+    import paper_2004_09883_b200 as m
+    torch.cuda.set_device(0)
+    m.fb_init(0)
+    return m
+
+
+def _bar(n0, n1):
+    return 1e-5 * max(1.0, np.log2(n0 * n1))
+
+
+def _run(fb, x, inverse=False, inplace=False):
+    xd = torch.from_numpy(np.ascontiguousarray(x)).cuda()
+    if inplace:
+        fb.fft2d(xd, out=xd, inverse=inverse)
+        out = xd
+    else:
+        out = fb.fft2d(xd, inverse=inverse)
+    torch.cuda.synchronize()
+    return out.cpu().numpy()
+
+
+SMALL = [1, 2, 4, 8, 16, 32, 64, 128]
+
+
+@pytest.mark.parametrize("n0,n1", list(itertools.product(SMALL, SMALL)))
+def test_small_all_shapes_vs_oracle(fb, n0, n1):
+    x = synth.complex_field(n0, n1, tensor_id=n0 * 1000 + n1)
+    for inv in (False, True):
+        y = _run(fb, x, inverse=inv)
+        ref = oracle.dft2d(x, inverse=inv)
+        err = oracle.rel_l2(y, ref)
+        assert err < min(_bar(n0, n1), 5e-7), (n0, n1, inv, err)
+
+
+@pytest.mark.parametrize("n0,n1", [(256, 256), (512, 256), (256, 1024), (1024, 64), (64, 2048)])
+def test_full_oracle(fb, n0, n1):
+    x = synth.complex_field(n0, n1)
+    ref = oracle.dft2d(x)
+    y = _run(fb, x)
+    assert oracle.rel_l2(y, ref) < 5e-7
+    z = _run(fb, y.astype(np.complex64), inverse=True)
+    assert oracle.rel_l2(z, oracle.dft2d(y.astype(np.complex64), inverse=True)) < 5e-7
+
+
+def test_256_forward_inverse_config0(fb):
+    """BASELINE configs[0]: 256x256 fp32, single forward + inverse."""
+    x = synth.complex_field(256, 256)
+    y = _run(fb, x)
+    assert oracle.rel_l2(y, oracle.dft2d(x)) < 5e-7
+    z = _run(fb, y, inverse=True)
+    assert oracle.rel_l2(z, x) < 5e-7
+
+
+def test_inplace_equals_out_of_place(fb):
+    x = synth.complex_field(512, 512)
+    a = _run(fb, x)
+    b = _run(fb, x, inplace=True)
+    assert np.array_equal(a, b)
+
+
+def test_deterministic(fb):
+    x = synth.complex_field(1024, 1024)
+    assert np.array_equal(_run(fb, x), _run(fb, x))
+
+
+def _sampled_check(fb, n0, n1, x, y, ks0, ks1, inverse=False, tol=5e-7):
+    for k1 in ks1:
+        ref = oracle.dft2d_col(x, k1, inverse=inverse)
+        assert oracle.rel_l2(y[:, k1], ref) < tol, ("col", k1)
+    for k0 in ks0:
+        ref = oracle.dft2d_row(x, k0, inverse=inverse)
+        assert oracle.rel_l2(y[k0, :], ref) < tol, ("row", k0)
+
+
+def test_2048_config1_sampled_and_closed_forms(fb):
+    """BASELINE configs[1]: 2048x2048 -- sampled full rows/columns vs the oracle, plus
+    Parseval and roundtrip at full size."""
+    n = 2048
+    x = synth.complex_field(n, n)
+    y = _run(fb, x)
+    _sampled_check(fb, n, n, x, y, [0, 1, 1023, 2047], [0, 5, 1024, 2047])
+    xs = x.astype(np.complex128)
+    assert np.isclose(np.sum(np.abs(y.astype(np.complex128)) ** 2), n * n * np.sum(np.abs(xs) ** 2), rtol=1e-5)
+    z = _run(fb, y, inverse=True)
+    assert oracle.rel_l2(z, x) < 5e-7
+
+
+def test_2048_tones(fb):
+    """Paper-shaped input (P:149 vibration analysis): integer tones + noise; the spectrum
+    peaks sit exactly at the tone frequencies."""
+    n = 2048
+    x, tones = synth.tones2d(n, n)
+    y = _run(fb, x)
+    mag = np.abs(y)
+    top = set(zip(*np.unravel_index(np.argsort(mag.ravel())[-len(tones):], mag.shape)))
+    assert {(f0, f1) for f0, f1, _ in tones} == {(int(a), int(b)) for a, b in top}
+    for k1 in sorted({f1 for _, f1, _ in tones})[:3]:
+        assert oracle.rel_l2(y[:, k1], oracle.dft2d_col(x, k1)) < 1e-5
+
+
+@pytest.mark.parametrize("n0,n1", [(8192, 64), (16384, 32), (8192, 256)])
+def test_four_step_columns(fb, n0, n1):
+    x = synth.complex_field(n0, n1)
+    y = _run(fb, x)
+    _sampled_check(fb, n0, n1, x, y, [0, 3, n0 - 1], [0, 7, n1 - 1])
+    z = _run(fb, y, inverse=True)
+    assert oracle.rel_l2(z, x) < 5e-7
+
+
+def test_16384_square_sampled(fb):
+    """configs[3] size on one GPU: 16384 x 16384 (2 GiB), sampled lines + tone closed form."""
+    n = 16384
+    x = synth.complex_field(n, n)
+    y = _run(fb, x)
+    _sampled_check(fb, n, n, x, y, [0, n - 1], [0, 8191], tol=1e-6)
+    # single tone: exact spike at (f0, f1)
+    f0, f1 = 1234, 15000
+    i = np.arange(n, dtype=np.int64)
+    r0 = np.exp(2j * np.pi * ((f0 * i) % n) / n).astype(np.complex64)
+    r1 = np.exp(2j * np.pi * ((f1 * i) % n) / n).astype(np.complex64)
+    tone = r0[:, None] * r1[None, :]
+    yt = _run(fb, tone)
+    assert abs(yt[f0, f1] - n * n) < 1e-4 * n * n
+    yt[f0, f1] = 0
+    assert np.abs(yt).max() < 1e-4 * n * n
+
+
+def test_delta_closed_form_gpu(fb):
+    n0, n1, a, b = 1024, 512, 77, 301
+    x = np.zeros((n0, n1), np.complex64)
+    x[a, b] = 1
+    y = _run(fb, x)
+    k0 = np.arange(n0)[:, None]
+    k1 = np.arange(n1)[None, :]
+    ref = np.exp(-2j * np.pi * ((k0 * a % n0) / n0 + (k1 * b % n1) / n1))
+    assert np.abs(y - ref).max() < 2e-6
+
+
+def test_host_variant(fb):
+    x = synth.complex_field(512, 256)
+    xh = torch.from_numpy(x).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+    fb.fb_fft2d_host(xh, yh)
+    assert oracle.rel_l2(yh.numpy(), oracle.dft2d(x)) < 5e-7
+    fb.fb_fft2d_host(yh, xh, inverse=True)
+    assert oracle.rel_l2(xh.numpy(), x) < 5e-7
