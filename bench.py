@@ -12,7 +12,7 @@ roofline; so are the 256^2 forward+inverse (configs[0]) and the single-GPU 16384
 configs[3]: the slab-sharded 16384^2 FFT with its NCCL all-to-all (strong scaling).
 
 Timing: inputs resident in HBM; before every timed step L2 is flushed by a 512 MiB memset
-(untimed); each step is bracketed by CUDA events on the launching stream; barrier +
+followed by a 1 GiB read (untimed; leaves L2 clean); each step is bracketed by CUDA events on the launching stream; barrier +
 synchronize around the timed region; max over ranks.  FLOP conventions: FFT 5 N log2 N
 (N = n0 n1), GEMM 2 M N K.  The `--impl reference` arm times the CPU oracle (oracle/) on a
 bounded sample of the same workload.
@@ -224,9 +224,13 @@ def main():
     stream = torch.cuda.Stream()
     pk = peaks()
     flush_buf = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
+    clean_buf = torch.ones(FLUSH_BYTES // 2, dtype=torch.int32, device="cuda")
 
     def flush():
+        # write 512 MiB (> 126 MB L2) then read 1 GiB so that L2 holds only clean lines:
+        # the flush's own dirty lines are not written back inside the next timed step
         flush_buf.zero_()
+        clean_buf.sum()
 
     only = set(filter(None, args.only.split(",")))
     out = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -251,7 +255,7 @@ def main():
         achieved = bytes_launch / ((t / launches) * 1e-3) / 1e9
         out.update({"value": gflops, "unit": "GFLOP/s", "ms_per_step": t, "scaling": "strong",
                     "config": {"workload": "fft2d_2048x2048_fwd", "n0": n, "n1": n, "element": "complex64",
-                               "l2": "flushed (512 MiB memset, untimed) before every timed step",
+                               "l2": "flushed before every timed step (untimed): 512 MiB memset + 1 GiB read",
                                "configs_index": 1},
                     "roofline": {"bound": "hbm", "kernel": "fft_pass_kernel (row pass + column pass)",
                                  "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
@@ -270,7 +274,9 @@ def main():
             ets = []
             for _ in range(args.steps):
                 a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                flush()
+                with torch.cuda.stream(stream):
+                    flush()
+                torch.cuda.synchronize()
                 a.record(stream)
                 fb.fb_fft2d_host(xh, yh, stream=stream)
                 b.record(stream)

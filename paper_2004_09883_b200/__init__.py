@@ -16,7 +16,7 @@ import os
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfb.so")
+LIB_PATH = os.environ.get("FB_LIB", os.path.join(_HERE, "libfb.so"))  # FB_LIB: experiment builds
 
 FB_F32 = 0
 FB_F64 = 1

@@ -21,38 +21,66 @@
 // Stockham autosort (mixed radix): stage with radix R after Ns = product of earlier radices,
 // butterfly j reads x[j + r L/R] (r < R), multiplies by W_{Ns R}^{(j mod Ns) r}, applies the
 // radix-R DFT, writes y[(j / Ns) Ns R + (j mod Ns) + r Ns].  Output is in natural order.
+#include <cuda.h>
+#include <stdlib.h>
+#include <string.h>
+
 #include "fb_common.cuh"
+#include "fb_ptx.cuh"
 
 namespace fb {
 
-__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
-    return make_float2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+// Complex arithmetic on interleaved (re, im) pairs with the sm_100 packed-FP32 instructions
+// (FADD2 / FMUL2 / FFMA2; operand broadcast, lane swap and per-lane negation are free
+// operand modifiers), so a complex add is one instruction and a complex multiply two.
+// Every lane is IEEE RN, identical to the scalar forms.
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __ffma2_rn(b, bc2(-1.f), a); }
+// a * w  = a.x (w.x, w.y) + a.y (-w.y, w.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+    const float2 t = __fmul2_rn(bc2(a.x), w);
+    return __ffma2_rn(make_float2(-w.y, w.x), bc2(a.y), t);
 }
-__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
+// a + (-i) b = (a.x + b.y, a.y - b.x)   and   a - (-i) b = (a.x - b.y, a.y + b.x)
+__device__ __forceinline__ float2 cadd_mi(float2 a, float2 b) {
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(1.f, -1.f), a);
+}
+__device__ __forceinline__ float2 csub_mi(float2 a, float2 b) {
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a);
+}
+// x * (c - i s) = c x + s (x.y, -x.x)
+__device__ __forceinline__ float2 cmul_cs(float2 x, float c, float s) {
+    const float2 t = __fmul2_rn(x, bc2(c));
+    return __ffma2_rn(make_float2(x.y, x.x), make_float2(s, -s), t);
+}
 
-// x * exp(-2 pi i K / R) for 0 <= K < R/2 with compile-time K, R <= 16.
-// Multiples of pi/4 are applied exactly (swaps / one scalar), the rest with RN constants.
+// Radix-2 combine of the DIT recursion with the compile-time twiddle W_R^K = exp(-2 pi i K/R):
+// v[K] = e + W o, v[K + R/2] = e - W o.  K = 0 and K = R/4 (-i) need no multiply.
 template <int K, int R>
-__device__ __forceinline__ float2 mul_wR(float2 x) {
-    constexpr float kS = 0.707106781186547524400844362104849039f;  // cos(pi/4)
+__device__ __forceinline__ void butterfly(float2* v, float2 e, float2 o) {
+    constexpr float kS = 0.707106781186547524400844362104849039f;   // cos(pi/4)
     constexpr float kC1 = 0.923879532511286756128183189396788933f;  // cos(pi/8)
     constexpr float kS1 = 0.382683432365089771728459984030398866f;  // sin(pi/8)
     if constexpr (K == 0) {
-        return x;
-    } else if constexpr (4 * K == R) {  // -i
-        return make_float2(x.y, -x.x);
-    } else if constexpr (8 * K == R) {  // exp(-i pi/4)
-        return make_float2((x.x + x.y) * kS, (x.y - x.x) * kS);
-    } else if constexpr (8 * K == 3 * R) {  // exp(-3 i pi/4)
-        return make_float2((x.y - x.x) * kS, -(x.x + x.y) * kS);
+        v[K] = cadd(e, o);
+        v[K + R / 2] = csub(e, o);
+    } else if constexpr (4 * K == R) {
+        v[K] = cadd_mi(e, o);
+        v[K + R / 2] = csub_mi(e, o);
     } else {
-        static_assert(R == 16, "only R=16 needs pi/8 constants");
-        // theta = 2 pi K / 16 = K pi / 8 with K odd in {1,3,5,7}
-        constexpr float c = (K == 1) ? kC1 : (K == 3) ? kS1 : (K == 5) ? -kS1 : -kC1;
-        constexpr float s = (K == 1) ? kS1 : (K == 3) ? kC1 : (K == 5) ? kC1 : kS1;
-        // x * (c - i s)
-        return make_float2(x.x * c + x.y * s, x.y * c - x.x * s);
+        // theta = 2 pi K / R in (0, pi), K != R/4; cos/sin as RN FP32 constants
+        constexpr float c = (8 * K == R) ? kS : (8 * K == 3 * R) ? -kS
+                          : (16 * K == R) ? kC1 : (16 * K == 3 * R) ? kS1
+                          : (16 * K == 5 * R) ? -kS1 : -kC1;
+        constexpr float s = (8 * K == R || 8 * K == 3 * R) ? kS
+                          : (16 * K == R || 16 * K == 7 * R) ? kS1 : kC1;
+        static_assert(8 * K == R || 8 * K == 3 * R || 16 * K == R || 16 * K == 3 * R || 16 * K == 5 * R ||
+                          16 * K == 7 * R,
+                      "radix > 16 not supported");
+        const float2 t = cmul_cs(o, c, s);
+        v[K] = cadd(e, t);
+        v[K + R / 2] = csub(e, t);
     }
 }
 
@@ -60,9 +88,7 @@ template <int R, int K>
 struct Combine {
     __device__ __forceinline__ static void run(float2* v, const float2* e, const float2* o) {
         if constexpr (K < R / 2) {
-            float2 tt = mul_wR<K, R>(o[K]);
-            v[K] = cadd(e[K], tt);
-            v[K + R / 2] = csub(e[K], tt);
+            butterfly<K, R>(v, e[K], o[K]);
             Combine<R, K + 1>::run(v, e, o);
         }
     }
@@ -74,7 +100,7 @@ __device__ __forceinline__ void dft(float2* v) {
     if constexpr (R == 1) {
         return;
     } else if constexpr (R == 2) {
-        float2 a = v[0], b = v[1];
+        const float2 a = v[0], b = v[1];
         v[0] = cadd(a, b);
         v[1] = csub(a, b);
     } else {
@@ -106,9 +132,9 @@ struct LineGeom {
 __host__ __device__ constexpr int padk(int k) { return k + (k >> 4); }
 
 // ---- per-stage twiddle tables (built once per device by fb_init, see stage_tw_index()):
-// for line length 2^l and stage s >= 1 (radix R, Ns = 16^s), entries [jm][r] = W_{Ns R}^{jm r},
-// jm < Ns, r < R, stored contiguously so a thread fetches its R twiddles with R/2 16-byte
-// loads at immediate offsets from one base pointer.
+// for line length 2^l and stage s >= 1 (radix R, Ns = 16^s), entries [r][jm] = W_{Ns R}^{jm r},
+// r < R, jm < Ns: a warp's lanes (consecutive jm) read consecutive entries for each r, and a
+// thread reaches its R twiddles at immediate offsets r*Ns from one base pointer.
 __host__ __device__ constexpr int stage_radix(int l, int s) {
     return (s < (l >= 4 ? l / 4 : 0)) ? 16 : (1 << (l >= 4 ? l % 4 : l));
 }
@@ -134,8 +160,8 @@ void stage_tw_index(int32_t* idx) {
             const int R = stage_radix(l, s);
             const int64_t Ns = int64_t(1) << (4 * s);
             const int64_t step = kTwN / (Ns * R);
-            for (int64_t jm = 0; jm < Ns; ++jm)
-                for (int r = 0; r < R; ++r) idx[e++] = (int32_t)(jm * r * step);
+            for (int r = 0; r < R; ++r)
+                for (int64_t jm = 0; jm < Ns; ++jm) idx[e++] = (int32_t)(jm * r * step);
         }
 }
 
@@ -171,15 +197,11 @@ struct Stages {
 #pragma unroll
                 for (int r = 0; r < R; ++r) b[r] = v[q + r * Q];
                 if constexpr (!first) {
+                    // table layout [r][jm]: lanes with consecutive jm read consecutive entries
                     const int jm = (t + q * T) & (Ns - 1);
-                    const float4* tw4 = reinterpret_cast<const float4*>(
-                        stw + stage_tw_offset(LOG2L, S) + (int64_t)jm * R);
+                    const float2* twp = stw + stage_tw_offset(LOG2L, S) + jm;
 #pragma unroll
-                    for (int r2 = 0; r2 < R / 2; ++r2) {
-                        const float4 w = __ldg(tw4 + r2);
-                        if (r2 > 0) b[2 * r2] = cmul(b[2 * r2], make_float2(w.x, w.y));
-                        b[2 * r2 + 1] = cmul(b[2 * r2 + 1], make_float2(w.z, w.w));
-                    }
+                    for (int r = 1; r < R; ++r) b[r] = cmul(b[r], __ldg(twp + r * Ns));
                 }
                 dft<R>(b);
 #pragma unroll
@@ -206,10 +228,19 @@ struct Stages {
     }
 };
 
-// PLAIN: both line maps unblocked (element k at k*es) -> incremental 64-bit addressing.
-template <int LOG2L, int C, bool PLAIN>
+// MODE (addressing of the global loads/stores):
+//   1: both maps unblocked with unit element stride (rows): compile-time offsets;
+//   2: both maps unblocked, strided elements (columns): pointer increments;
+//   0: general LineMap (per-peer blocks of the slab all-to-all).
+#ifndef FB_FFT_THREADS_PER_SM
+#define FB_FFT_THREADS_PER_SM 1024  // occupancy target -> register cap 65536 / this
+#endif
+template <int LOG2L, int C, int MODE>
 __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
-                                  (C * LineGeom<LOG2L>::T >= 1024) ? 1 : 1024 / (C * LineGeom<LOG2L>::T))
+                                  (C * LineGeom<LOG2L>::T >= FB_FFT_THREADS_PER_SM) ? 1
+                                  : (FB_FFT_THREADS_PER_SM / (C * LineGeom<LOG2L>::T) > 32)
+                                      ? 32
+                                      : FB_FFT_THREADS_PER_SM / (C * LineGeom<LOG2L>::T))
     fft_pass_kernel(const FftPass p, const float2* __restrict__ tw, const float2* __restrict__ stw) {
     using G = LineGeom<LOG2L>;
     extern __shared__ float2 sm[];
@@ -225,11 +256,18 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
     float2* dst = p.out + gh * p.lout.hi + gl * p.lout.lo;
 
     float2 v[G::E];
-    if constexpr (PLAIN) {
-        const float2* sp = src + (int64_t)t * p.lin.es;
-        const int64_t sstride = (int64_t)G::T * p.lin.es;
+    if constexpr (MODE == 1) {
+        const float2* sp = src + t;
 #pragma unroll
-        for (int m = 0; m < G::E; ++m) v[m] = valid ? sp[m * sstride] : make_float2(0.f, 0.f);
+        for (int m = 0; m < G::E; ++m) v[m] = valid ? sp[m * G::T] : make_float2(0.f, 0.f);
+    } else if constexpr (MODE == 2) {
+        const char* sp = reinterpret_cast<const char*>(src + (int64_t)t * p.lin.es);
+        const int64_t step = (int64_t)G::T * p.lin.es * (int64_t)sizeof(float2);
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            v[m] = valid ? *reinterpret_cast<const float2*>(sp) : make_float2(0.f, 0.f);
+            sp += step;
+        }
     } else {
         const int in_kmask = (1 << p.lin.kb_shift) - 1;
 #pragma unroll
@@ -268,11 +306,18 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
             v[m].y *= p.scale;
         }
     }
-    if constexpr (PLAIN) {
-        float2* dp = dst + (int64_t)t * p.lout.es;
-        const int64_t dstride = (int64_t)G::T * p.lout.es;
+    if constexpr (MODE == 1) {
+        float2* dp = dst + t;
 #pragma unroll
-        for (int m = 0; m < G::E; ++m) dp[m * dstride] = v[m];
+        for (int m = 0; m < G::E; ++m) dp[m * G::T] = v[m];
+    } else if constexpr (MODE == 2) {
+        char* dp = reinterpret_cast<char*>(dst + (int64_t)t * p.lout.es);
+        const int64_t step = (int64_t)G::T * p.lout.es * (int64_t)sizeof(float2);
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            *reinterpret_cast<float2*>(dp) = v[m];
+            dp += step;
+        }
     } else {
         const int out_kmask = (1 << p.lout.kb_shift) - 1;
 #pragma unroll
@@ -284,7 +329,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
     }
 }
 
-template <int LOG2L, int C, bool PLAIN>
+template <int LOG2L, int C, int MODE>
 static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     using G = LineGeom<LOG2L>;
     constexpr int threads = C * G::T;
@@ -294,7 +339,7 @@ static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_
     int dev = 0;
     cudaGetDevice(&dev);
     if (smem > 48 * 1024 && !(attr_done_mask & (1 << (dev & 31)))) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(fft_pass_kernel<LOG2L, C, PLAIN>,
+        FB_CUDA_TRY(cudaFuncSetAttribute(fft_pass_kernel<LOG2L, C, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_done_mask |= 1 << (dev & 31);
     }
@@ -303,7 +348,7 @@ static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_
         set_error("FFT pass grid too large (%lld CTAs)", (long long)blocks);
         return FB_ERR_UNSUPPORTED_SIZE;
     }
-    fft_pass_kernel<LOG2L, C, PLAIN><<<(unsigned)blocks, threads, smem, s>>>(p, st->twiddles, st->stage_tw);
+    fft_pass_kernel<LOG2L, C, MODE><<<(unsigned)blocks, threads, smem, s>>>(p, st->twiddles, st->stage_tw);
     FB_LAUNCH_CHECK("fft_pass_kernel");
     return FB_OK;
 }
@@ -311,7 +356,9 @@ static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_
 template <int LOG2L, int C>
 static fb_status launch_LC(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     const bool plain = p.lin.kb_shift >= LOG2L && p.lout.kb_shift >= LOG2L;
-    return plain ? launch_one<LOG2L, C, true>(p, st, s) : launch_one<LOG2L, C, false>(p, st, s);
+    if (plain && p.lin.es == 1 && p.lout.es == 1) return launch_one<LOG2L, C, 1>(p, st, s);
+    if (plain) return launch_one<LOG2L, C, 2>(p, st, s);
+    return launch_one<LOG2L, C, 0>(p, st, s);
 }
 
 template <int LOG2L>
@@ -349,8 +396,340 @@ static int pick_C(int log2L, bool col_like) {
     return C;
 }
 
+// =====================================================================================
+// Persistent, TMA-pipelined pass (the fast path).  Each CTA loops over groups of C lines;
+// while group i is transformed, the async proxy is already filling the other staging buffer
+// with group i+1 (two staging buffers, one mbarrier each), so global-load latency is hidden
+// and no LSU instruction touches the strided input:
+//   KIND_ROW: lines (or per-peer line segments) are contiguous -> 1D bulk copies
+//             (cp.async.bulk) into S[c][k]; outputs leave by coalesced direct stores.
+//   KIND_COL: lines are adjacent columns -> one 3D TMA tensor box per 256 elements into
+//             S[k][c] (32 B or 16 B row segments gathered by the TMA engine); outputs are
+//             written densely to the exchange buffer and leave by TMA tensor stores.
+// Stage 1 reads S, later stages exchange through the padded buffer X exactly as in
+// fft_pass_kernel (same arithmetic, same results bit for bit).
+// =====================================================================================
+enum { KIND_ROW = 1, KIND_COL = 2 };
+
+template <int LOG2L, int C, int KIND>
+struct TmaGeom {
+    using G = LineGeom<LOG2L>;
+    static constexpr int PADS = (KIND == KIND_ROW && C > 1) ? 16 / C : 0;  // S line pad (row kind)
+    static constexpr int SLINE = G::L + PADS;
+    static constexpr int S_ELEMS = (KIND == KIND_ROW) ? C * SLINE : C * G::L;
+    static constexpr int X_ELEMS = C * G::PADL;
+    static constexpr size_t SMEM = (size_t)(2 * S_ELEMS + X_ELEMS) * sizeof(float2) + 64;
+    static constexpr int BOX = G::L < 256 ? G::L : 256;  // COL: elements per TMA box
+};
+
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC>
+__global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, 1)
+    fft_pass_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap tin,
+                        const __grid_constant__ CUtensorMap tout, const float2* __restrict__ tw,
+                        const float2* __restrict__ stw, int64_t ngroups, int64_t nh_in) {
+    using G = LineGeom<LOG2L>;
+    using TG = TmaGeom<LOG2L, C, KIND>;
+    constexpr int L = G::L, T = G::T, E = G::E;
+    extern __shared__ __align__(128) float2 smf[];
+    float2* Sbuf = smf;
+    float2* X = smf + 2 * TG::S_ELEMS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(X + TG::X_ELEMS);
+    const int tid = threadIdx.x;
+    const int c = tid % C;
+    const int t = tid / C;
+    const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+    const int64_t gmask = (gshift >= 62) ? -1 : ((int64_t(1) << gshift) - 1);
+
+    if (tid == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bars[0]), 1);
+        ptx::mbar_init(ptx::smem_u32(&bars[1]), 1);
+        ptx::fence_mbar_init();
+        if constexpr (KIND == KIND_COL) {
+            ptx::tma_prefetch_desc(&tin);
+            ptx::tma_prefetch_desc(&tout);
+        }
+    }
+    __syncthreads();
+
+    // thread 0: start the asynchronous fill of staging buffer `buf` with group `grp`
+    auto issue = [&](int64_t grp, int buf) {
+        float2* S = Sbuf + buf * TG::S_ELEMS;
+        const uint32_t bar = ptx::smem_u32(&bars[buf]);
+        const int64_t g0 = grp * C;
+        if constexpr (KIND == KIND_COL) {
+            ptx::mbar_arrive_expect_tx(bar, (uint32_t)(C * L * sizeof(float2)));
+            const int64_t gh = (gshift >= 62) ? 0 : (g0 >> gshift);
+            const int gl = (int)(g0 & gmask);
+#pragma unroll 1
+            for (int kb = 0; kb < L; kb += TG::BOX)
+                ptx::tma_load_3d(ptx::smem_u32(S + kb * C), &tin, bar, gl, kb, (int)gh);
+        } else {
+            const int64_t nv = (p.nlines - g0) < C ? (p.nlines - g0) : C;
+            const int seg = (p.lin.kb_shift >= LOG2L) ? L : (1 << p.lin.kb_shift);
+            ptx::mbar_arrive_expect_tx(bar, (uint32_t)(nv * L * sizeof(float2)));
+            for (int cl = 0; cl < nv; ++cl) {
+                const int64_t g = g0 + cl;
+                const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
+                const float2* src = p.in + gh * p.lin.hi + (g & gmask) * p.lin.lo;
+#pragma unroll 1
+                for (int k0 = 0; k0 < L; k0 += seg)
+                    ptx::bulk_load(ptx::smem_u32(S + cl * TG::SLINE + k0), src + (int64_t)(k0 / seg) * p.lin.bs,
+                                   (uint32_t)(seg * sizeof(float2)), bar);
+            }
+        }
+    };
+
+    if (tid == 0) {
+        if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+        if ((int64_t)blockIdx.x + gridDim.x < ngroups) issue((int64_t)blockIdx.x + gridDim.x, 1);
+    }
+    (void)nh_in;
+
+    int it = 0;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+        const int buf = it & 1;
+        const float2* S = Sbuf + buf * TG::S_ELEMS;
+        ptx::mbar_wait(ptx::smem_u32(&bars[buf]), (uint32_t)(it >> 1) & 1u);
+        float2 v[E];
+        if constexpr (KIND == KIND_COL) {
+            const float2* sp = S + t * C + c;
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = sp[m * T * C];
+        } else {
+            const float2* sp = S + c * TG::SLINE + t;
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = sp[m * T];
+        }
+        if (p.conj_in) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
+        }
+        // order this thread's generic-proxy reads of S[buf] before the async-proxy (TMA)
+        // refill of S[buf] that thread 0 issues after the barrier
+        ptx::fence_proxy_async_smem();
+        if constexpr (KIND == KIND_COL) {
+            if (tid == 0) ptx::bulk_wait_read0();  // previous group's TMA store has read X
+        }
+        __syncthreads();  // S[buf] consumed by everyone; X free
+        if (tid == 0) {
+            const int64_t nxt = grp + 2 * (int64_t)gridDim.x;
+            if (nxt < ngroups) issue(nxt, buf);
+        }
+
+        Stages<LOG2L, C, 0>::run(v, X, t, c, stw);
+
+        const int64_t g = grp * C + c;
+        const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
+        if (p.tw4_log2N > 0) {
+            const int tw4 = p.tw4_log2N;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k = t + m * T;
+                const int64_t e = (gh * (int64_t)k) & ((int64_t(1) << tw4) - 1);
+                v[m] = cmul(v[m], __ldg(tw + (e << (kTwLog2 - tw4))));
+            }
+        }
+        if (p.conj_out) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
+        }
+        if (p.scale != 1.0f) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = __fmul2_rn(v[m], bc2(p.scale));
+        }
+        if constexpr (KIND == KIND_COL) {
+            __syncthreads();  // last stage finished reading X
+            float2* xp = X + t * C + c;
+#pragma unroll
+            for (int m = 0; m < E; ++m) xp[m * T * C] = v[m];
+            ptx::fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                const int64_t g0 = grp * C;
+                const int64_t gh0 = (gshift >= 62) ? 0 : (g0 >> gshift);
+                const int gl0 = (int)(g0 & gmask);
+#pragma unroll 1
+                for (int kb = 0; kb < L; kb += TG::BOX)
+                    ptx::tma_store_3d(&tout, ptx::smem_u32(X + kb * C), gl0, kb, (int)gh0);
+                ptx::bulk_commit();
+            }
+        } else {
+            if (g < p.nlines) {
+                float2* dst = p.out + gh * p.lout.hi + (g & gmask) * p.lout.lo;
+                if constexpr (!OUT_GENERIC) {
+                    float2* dp = dst + t;
+#pragma unroll
+                    for (int m = 0; m < E; ++m) dp[m * T] = v[m];
+                } else {
+                    const int out_kmask = (1 << p.lout.kb_shift) - 1;
+#pragma unroll
+                    for (int m = 0; m < E; ++m) {
+                        const int k = t + m * T;
+                        dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] =
+                            v[m];
+                    }
+                }
+            }
+        }
+    }
+    if constexpr (KIND == KIND_COL) {
+        if (tid == 0) ptx::bulk_wait0();
+    }
+}
+
+// ------------------------------------------------------------ host side of the TMA path
+typedef CUresult (*EncodeTiledFnFFT)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFnFFT fft_encoder() {
+    static EncodeTiledFnFFT fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFnFFT)f;
+    }
+    return fn;
+}
+
+// 3D view {line-lo (contiguous lines), element k (stride es), line-hi (stride hi)} of 8-byte
+// complex elements; box {C, min(L,256), 1}.
+static bool make_col_map(CUtensorMap* m, const void* base, int64_t glo, int64_t L, int64_t nh, int64_t es,
+                         int64_t hi, int C) {
+    EncodeTiledFnFFT enc = fft_encoder();
+    if (!enc) return false;
+    if (nh <= 1) hi = es * L;  // unused dimension; any legal stride
+    cuuint64_t dims[3] = {(cuuint64_t)glo, (cuuint64_t)L, (cuuint64_t)(nh < 1 ? 1 : nh)};
+    cuuint64_t strides[2] = {(cuuint64_t)(es * 8), (cuuint64_t)(hi * 8)};
+    cuuint32_t box[3] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC>
+static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    using TG = TmaGeom<LOG2L, C, KIND>;
+    constexpr int threads = C * LineGeom<LOG2L>::T;
+    auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC>;
+    static int attr_done_mask = 0;
+    static int occ[32] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done_mask & (1 << (dev & 31)))) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG::SMEM));
+        int nb = 0;
+        FB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, TG::SMEM));
+        occ[dev & 31] = nb < 1 ? 1 : nb;
+        attr_done_mask |= 1 << (dev & 31);
+    }
+    const int64_t ngroups = (p.nlines + C - 1) / C;
+    int64_t grid = (int64_t)st->sm_count * occ[dev & 31];
+    if (grid > ngroups) grid = ngroups;
+    CUtensorMap tin, tout;
+    memset(&tin, 0, sizeof(tin));
+    memset(&tout, 0, sizeof(tout));
+    int64_t nh = 1;
+    if (KIND == KIND_COL) {
+        const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+        const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
+        nh = (p.nlines + glo - 1) / glo;
+        if (!make_col_map(&tin, p.in, glo, int64_t(1) << LOG2L, nh, p.lin.es, p.lin.hi, C) ||
+            !make_col_map(&tout, p.out, glo, int64_t(1) << LOG2L, nh, p.lout.es, p.lout.hi, C)) {
+            set_error("cuTensorMapEncodeTiled failed for an FFT column pass");
+            return FB_ERR_CUDA;
+        }
+    }
+    kern<<<(unsigned)grid, threads, TG::SMEM, s>>>(p, tin, tout, st->twiddles, st->stage_tw, ngroups, nh);
+    FB_LAUNCH_CHECK("fft_pass_tma_kernel");
+    return FB_OK;
+}
+
+// Tuning knobs read once from the environment (for A/B measurements; defaults are the tuned
+// configuration).
+static int fft_knob(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+
+// Picks the TMA path when the pass is expressible; returns false to fall back.
+static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic) {
+    const int l = p.log2L;
+    if (l < 6 || l > 12) return false;  // >= 64 elements, staging fits for <= 4096
+    const bool al_in = ((uintptr_t)p.in & 15) == 0, al_out = ((uintptr_t)p.out & 15) == 0;
+    if (!al_in || !al_out) return false;
+    const bool in_plain = p.lin.kb_shift >= l, out_plain = p.lout.kb_shift >= l;
+    const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+    if (p.col_like && p.lin.lo == 1 && p.lout.lo == 1 && in_plain && out_plain) {
+        if (fft_knob("FB_FFT_NO_TMA_COL", 0)) return false;
+        // widest row segment (up to 128 B = 16 columns) whose double-buffered staging plus
+        // exchange buffer stays near 100 KiB (two CTAs per SM)
+        C = (l <= 8) ? 16 : (l == 9 ? 8 : (l == 10 ? 4 : 2));
+        const int kc = fft_knob("FB_FFT_COL_C", 0);
+        if (kc == 2 || kc == 4 || kc == 8 || kc == 16) C = kc;
+        if (C * (1 << l) / 16 > 1024 || (size_t)C * (1 << l) * 8 * 3 > 200 * 1024) return false;
+        const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
+        if (glo % C) return false;
+        if ((p.lin.es * 8) % 16 || (p.lout.es * 8) % 16) return false;
+        const int64_t nh = (p.nlines + glo - 1) / glo;
+        if (nh > 1 && ((p.lin.hi * 8) % 16 || (p.lout.hi * 8) % 16)) return false;
+        if (glo > (int64_t(1) << 31) || nh > (int64_t(1) << 31)) return false;
+        kind = KIND_COL;
+        out_generic = false;
+        return true;
+    }
+    if (!p.col_like && p.lin.es == 1 && p.lout.lo == 0 && p.lin.lo == 0) {
+        if (fft_knob("FB_FFT_NO_TMA_ROW", 0)) return false;
+        const int seg = in_plain ? (1 << l) : (1 << p.lin.kb_shift);
+        if (seg < 2) return false;
+        if ((p.lin.hi * 8) % 16) return false;
+        if (!in_plain && (p.lin.bs * 8) % 16) return false;
+        if (p.lout.es != 1) return false;
+        C = 1;
+        kind = KIND_ROW;
+        out_generic = !out_plain;
+        return true;
+    }
+    return false;
+}
+
+template <int LOG2L>
+static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const DeviceState* st, cudaStream_t s) {
+    constexpr int T = LineGeom<LOG2L>::T;
+    if (kind == KIND_COL) {
+        if (C == 2) return launch_tma_one<LOG2L, 2, KIND_COL, false>(p, st, s);
+        if (C == 4) return launch_tma_one<LOG2L, 4, KIND_COL, false>(p, st, s);
+        if constexpr (8 * T <= 1024 && LOG2L <= 11)
+            if (C == 8) return launch_tma_one<LOG2L, 8, KIND_COL, false>(p, st, s);
+        if constexpr (16 * T <= 1024 && LOG2L <= 10)
+            if (C == 16) return launch_tma_one<LOG2L, 16, KIND_COL, false>(p, st, s);
+    } else {
+        return og ? launch_tma_one<LOG2L, 1, KIND_ROW, true>(p, st, s)
+                  : launch_tma_one<LOG2L, 1, KIND_ROW, false>(p, st, s);
+    }
+    set_error("internal: no TMA FFT instantiation");
+    return FB_ERR_UNSUPPORTED_SIZE;
+}
+
+static bool g_fft_tma_disabled() { return fft_knob("FB_FFT_NO_TMA", 0) == 1; }
+
 fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     if (p.nlines <= 0) return FB_OK;
+    int kind = 0, tc = 0;
+    bool og = false;
+    if (!g_fft_tma_disabled() && tma_eligible(p, kind, tc, og)) {
+        switch (p.log2L) {
+            case 6: return launch_tma_L<6>(p, kind, tc, og, st, s);
+            case 7: return launch_tma_L<7>(p, kind, tc, og, st, s);
+            case 8: return launch_tma_L<8>(p, kind, tc, og, st, s);
+            case 9: return launch_tma_L<9>(p, kind, tc, og, st, s);
+            case 10: return launch_tma_L<10>(p, kind, tc, og, st, s);
+            case 11: return launch_tma_L<11>(p, kind, tc, og, st, s);
+            case 12: return launch_tma_L<12>(p, kind, tc, og, st, s);
+        }
+    }
     const int C = pick_C(p.log2L, p.col_like != 0);
     switch (p.log2L) {
         case 0: return launch_L<0>(p, C, st, s);
