@@ -224,13 +224,13 @@ def main():
     stream = torch.cuda.Stream()
     pk = peaks()
     flush_buf = torch.empty(FLUSH_BYTES, dtype=torch.uint8, device="cuda")
-    clean_buf = torch.ones(FLUSH_BYTES // 2, dtype=torch.int32, device="cuda")
+    clean_buf = torch.ones(FLUSH_BYTES // 2, dtype=torch.float32, device="cuda")  # 1 GiB
 
     def flush():
         # write 512 MiB (> 126 MB L2) then read 1 GiB so that L2 holds only clean lines:
         # the flush's own dirty lines are not written back inside the next timed step
         flush_buf.zero_()
-        clean_buf.sum()
+        clean_buf.sum()  # float32 reduction: reads only, no dtype-promotion copy
 
     only = set(filter(None, args.only.split(",")))
     out = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,

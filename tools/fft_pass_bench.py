@@ -21,7 +21,7 @@ y = torch.empty_like(x)
 ws_b = fb.lib().fb_fft2d_workspace_bytes(n0, n1)
 ws = torch.empty(max(ws_b, 1), dtype=torch.uint8, device="cuda") if ws_b else None
 flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
-clean = torch.ones(256 << 20, dtype=torch.uint8, device="cuda")
+clean = torch.ones(64 << 20, dtype=torch.float32, device="cuda")
 mode = os.environ.get("FLUSH", "write")  # none | write | write+read
 
 
@@ -30,7 +30,7 @@ def do_flush():
         return
     flush.zero_()
     if mode == "write+read":
-        torch.sum(clean.view(torch.int32))
+        clean.sum()
 s = torch.cuda.current_stream()
 ts = []
 for i in range(reps + 5):
