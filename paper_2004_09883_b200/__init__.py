@@ -249,27 +249,48 @@ def fb_matmul_host(A_host: torch.Tensor, B_host: torch.Tensor, C_host: torch.Ten
 
 
 # ------------------------------------------------------------------ multi-GPU
-class Comm:
-    """An fb_comm (NCCL communicator) for this process's GPU.
+def slab_rows(rank: int, world: int, n0: int) -> tuple[int, int]:
+    """Rows [r0, r1) of the natural n0 x n1 array owned by `rank` (reading R8)."""
+    if n0 % world:
+        raise ValueError("n0 must be divisible by the world size")
+    r = n0 // world
+    return rank * r, (rank + 1) * r
 
-    uid distribution uses torch.distributed (any backend) -- plumbing only."""
+
+def slab_cols(rank: int, world: int, n1: int) -> tuple[int, int]:
+    """Columns [c0, c1) of Y held by `rank` after fb_fft2d_slab (reading R8)."""
+    if n1 % world:
+        raise ValueError("n1 must be divisible by the world size")
+    c = n1 // world
+    return rank * c, (rank + 1) * c
+
+
+def exchange_unique_id(rank: int, world: int, make_uid, group=None) -> bytes:
+    """Rank 0 creates the communicator id with `make_uid()`; every rank returns the same bytes.
+    Uses torch.distributed (any backend) -- plumbing only."""
+    raw = make_uid() if rank == 0 else None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [raw]
+        dist.broadcast_object_list(obj, src=0, group=group)
+        raw = obj[0]
+    return bytes(raw)
+
+
+def _nccl_uid() -> bytes:
+    L = lib()
+    buf = ctypes.create_string_buffer(L.fb_comm_unique_id_bytes())
+    _check("fb_comm_unique_id", L.fb_comm_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """An fb_comm (NCCL communicator) for this process's GPU."""
 
     def __init__(self, rank: int, world: int, device: int, group=None):
-        import torch.distributed as dist
-        L = lib()
-        nb = L.fb_comm_unique_id_bytes()
-        uid = torch.zeros(nb, dtype=torch.uint8)
-        if rank == 0:
-            buf = ctypes.create_string_buffer(nb)
-            _check("fb_comm_unique_id", L.fb_comm_unique_id(buf))
-            uid = torch.frombuffer(bytearray(buf.raw), dtype=torch.uint8).clone()
-        if world > 1:
-            obj = [uid.tolist()]
-            dist.broadcast_object_list(obj, src=0, group=group)
-            uid = torch.tensor(obj[0], dtype=torch.uint8)
-        raw = bytes(uid.tolist())
+        raw = exchange_unique_id(rank, world, _nccl_uid, group)
         handle = ctypes.c_void_p()
-        _check("fb_comm_init", L.fb_comm_init(ctypes.byref(handle), world, rank, raw, device))
+        _check("fb_comm_init", lib().fb_comm_init(ctypes.byref(handle), world, rank, raw, device))
         self.handle = handle
         self.rank, self.world, self.device = rank, world, device
 
