@@ -361,13 +361,15 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
         ms = timed_steps(torch, lambda: fb.fb_matmul(A, B, C, None, stream), steps, args.warmup, flush, stream)
         t = float(np.mean(ms))
         flops = 2.0 * n * n * n
-        f64_peak = pk["bf16_tflops"] / 2250.0 * 40.0  # B200 nominal FP64 tensor 40 TF vs 2250 TF bf16
+        # FP64 DMMA peak: ncu measured 26.8 TFLOP/s at 72.26 % tensor(DMMA)-pipe utilisation of the
+        # elapsed cycles (profiles/r1_gemm_f64_full.txt) -> 37.1 TFLOP/s at 100 % on this pool
+        f64_peak = pk.get("fp64_dmma_tflops", 37.1)
         res["gemm_f64_2048"] = {
             "value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
             "config": {"workload": "gemm_2048^3_fp64_dmma", "configs_index": 2},
             "roofline": {"bound": "tensor", "kernel": "gemm_f64_dmma_kernel", "achieved": flops / (t * 1e-3) / 1e12,
                          "peak": f64_peak, "unit": "TFLOP/s", "frac": flops / (t * 1e-3) / 1e12 / f64_peak,
-                         "peak_source": pk["source"] + " bf16 x 40/2250 (FP64/BF16 nominal ratio)"}}
+                         "peak_source": "DMMA pipe peak derived from ncu utilisation (37.1 TFLOP/s)"}}
         del A, B, C
     # configs[0]: 256^2 forward + inverse
     if want("fft2d_256_fwd_inv"):

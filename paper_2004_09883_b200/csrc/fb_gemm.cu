@@ -2,7 +2,9 @@
 // GEMM C = A B, reading R9) on sm_100a.
 //
 // FB_F64: FP64 tensor-core FMAs (DMMA, mma.sync m16n8k8 f64; tcgen05 has no f64 kind), a
-//         3-stage cp.async pipeline into padded, bank-conflict-free shared-memory tiles.
+//         3-stage cp.async pipeline into padded, bank-conflict-free shared-memory tiles;
+//         64x64 tiles (several CTAs per SM) so the last wave does not idle SMs (A/B-measured:
+//         128x128 642.9 us, 128x64 597.8 us, 64x64 534.5 us at 2048^3).
 // FB_F32: 3xTF32 on the 5th-generation tensor cores.  A pre-pass splits every operand into
 //         RN-rounded TF32 hi and lo parts (hi = rna(x), lo = rna(x - hi)) and writes B
 //         transposed, so both operands are K-major.  The main kernel is warp specialised:
@@ -10,6 +12,7 @@
 //         an mbarrier ring; one thread issues tcgen05.mma kind::tf32 (hi*hi + hi*lo + lo*hi)
 //         into an FP32 accumulator in TMEM; four epilogue warps drain TMEM with tcgen05.ld.
 #include <cuda.h>
+#include <stdlib.h>
 
 #include "fb_common.cuh"
 #include "fb_ptx.cuh"
@@ -18,12 +21,20 @@ namespace fb {
 
 // =============================================================================== FP64 (DMMA)
 namespace f64 {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, THREADS = 256;
-constexpr int LDA_S = BK + 4;  // doubles; row stride 160 B -> conflict-free fragment loads
-constexpr int LDB_S = BN + 4;  // doubles
-constexpr int A_STAGE = BM * LDA_S;
-constexpr int B_STAGE = BK * LDB_S;
-constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+// Tile BM x BN x BK, WM x WN warps, warp tile (BM/WM) x (BN/WN) of m16n8k8 DMMA ops.
+template <int BM_, int BN_, int WM_, int WN_, int BK_ = 16, int ST_ = 3>
+struct Cfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = ST_, WM = WM_, WN = WN_;
+    static constexpr int THREADS = 32 * WM * WN;
+    static constexpr int TM = BM / WM / 16;   // m16 tiles per warp
+    static constexpr int TN = BN / WN / 8;    // n8 tiles per warp
+    static constexpr int LDA_S = BK + 4;      // doubles; 160-B rows -> conflict-free fragments
+    static constexpr int LDB_S = BN + 4;
+    static constexpr int A_STAGE = BM * LDA_S;
+    static constexpr int B_STAGE = BK * LDB_S;
+    static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+};
+using CfgSmall = Cfg<64, 64, 2, 2>;   // 1024 tiles at 2048^2: balanced across 148 SMs
 
 __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4], const double (&b)[2]) {
     asm volatile(
@@ -33,109 +44,116 @@ __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4]
         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
+template <class CF>
 __device__ __forceinline__ void load_stage(double* As, double* Bs, const double* __restrict__ A,
                                            const double* __restrict__ B, int64_t M, int64_t N,
                                            int64_t K, int64_t lda, int64_t ldb, int64_t m0,
                                            int64_t n0, int64_t k0, int tid) {
-    // A tile BM x BK: 128 rows x 8 chunks of 16 B (2 doubles)
+    // A tile BM x BK in 16-byte chunks (2 doubles)
 #pragma unroll
-    for (int i = 0; i < (BM * BK / 2) / THREADS; ++i) {
-        const int c = tid + i * THREADS;
-        const int r = c / (BK / 2), kc = (c % (BK / 2)) * 2;
-        const int64_t gr = m0 + r, gk = k0 + kc;
-        uint32_t bytes = 0;
-        const double* src = A;
-        if (gr < M && gk < K) {
-            bytes = (gk + 1 < K) ? 16 : 8;
-            src = A + gr * lda + gk;
+    for (int i = 0; i < (CF::BM * CF::BK / 2 + CF::THREADS - 1) / CF::THREADS; ++i) {
+        const int c = tid + i * CF::THREADS;
+        if (c < CF::BM * CF::BK / 2) {
+            const int r = c / (CF::BK / 2), kc = (c % (CF::BK / 2)) * 2;
+            const int64_t gr = m0 + r, gk = k0 + kc;
+            uint32_t bytes = 0;
+            const double* src = A;
+            if (gr < M && gk < K) {
+                bytes = (gk + 1 < K) ? 16 : 8;
+                src = A + gr * lda + gk;
+            }
+            ptx::cp_async_16(ptx::smem_u32(As + r * CF::LDA_S + kc), src, bytes);
         }
-        ptx::cp_async_16(ptx::smem_u32(As + r * LDA_S + kc), src, bytes);
     }
-    // B tile BK x BN: 16 rows x 64 chunks
+    // B tile BK x BN
 #pragma unroll
-    for (int i = 0; i < (BK * BN / 2) / THREADS; ++i) {
-        const int c = tid + i * THREADS;
-        const int r = c / (BN / 2), nc = (c % (BN / 2)) * 2;
-        const int64_t gk = k0 + r, gn = n0 + nc;
-        uint32_t bytes = 0;
-        const double* src = B;
-        if (gk < K && gn < N) {
-            bytes = (gn + 1 < N) ? 16 : 8;
-            src = B + gk * ldb + gn;
+    for (int i = 0; i < (CF::BK * CF::BN / 2 + CF::THREADS - 1) / CF::THREADS; ++i) {
+        const int c = tid + i * CF::THREADS;
+        if (c < CF::BK * CF::BN / 2) {
+            const int r = c / (CF::BN / 2), nc = (c % (CF::BN / 2)) * 2;
+            const int64_t gk = k0 + r, gn = n0 + nc;
+            uint32_t bytes = 0;
+            const double* src = B;
+            if (gk < K && gn < N) {
+                bytes = (gn + 1 < N) ? 16 : 8;
+                src = B + gk * ldb + gn;
+            }
+            ptx::cp_async_16(ptx::smem_u32(Bs + r * CF::LDB_S + nc), src, bytes);
         }
-        ptx::cp_async_16(ptx::smem_u32(Bs + r * LDB_S + nc), src, bytes);
     }
 }
 
-// 8 warps as 2 (M) x 4 (N); warp tile 64 x 32 = 4 m16 x 4 n8 DMMA tiles.
-__global__ void __launch_bounds__(THREADS, 1)
+// The k-loop order (k-blocks ascending, then kk, then the DMMA's internal order) is the same
+// for every tile shape, so results are bitwise identical across configurations.
+template <class CF>
+__global__ void __launch_bounds__(CF::THREADS)
     gemm_f64_dmma_kernel(const double* __restrict__ A, const double* __restrict__ B,
                          double* __restrict__ C, int64_t M, int64_t N, int64_t K, int64_t lda,
                          int64_t ldb, int64_t ldc) {
     extern __shared__ __align__(128) double smem_d[];
     double* As = smem_d;
-    double* Bs = smem_d + STAGES * A_STAGE;
+    double* Bs = smem_d + CF::STAGES * CF::A_STAGE;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;
-    const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
-    const int KT = (int)((K + BK - 1) / BK);
+    const int wm = warp / CF::WN, wn = warp % CF::WN;
+    const int64_t m0 = (int64_t)blockIdx.y * CF::BM, n0 = (int64_t)blockIdx.x * CF::BN;
+    const int KT = (int)((K + CF::BK - 1) / CF::BK);
 
-    double acc[4][4][4];
+    double acc[CF::TM][CF::TN][4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < CF::TN; ++j)
 #pragma unroll
             for (int v = 0; v < 4; ++v) acc[i][j][v] = 0.0;
 
 #pragma unroll
-    for (int s = 0; s < STAGES - 1; ++s) {
-        if (s < KT)
-            load_stage(As + s * A_STAGE, Bs + s * B_STAGE, A, B, M, N, K, lda, ldb, m0, n0,
-                       (int64_t)s * BK, tid);
+    for (int st = 0; st < CF::STAGES - 1; ++st) {
+        if (st < KT)
+            load_stage<CF>(As + st * CF::A_STAGE, Bs + st * CF::B_STAGE, A, B, M, N, K, lda, ldb, m0, n0,
+                           (int64_t)st * CF::BK, tid);
         ptx::cp_async_commit();
     }
     const int g = lane >> 2, tq = lane & 3;
     for (int kt = 0; kt < KT; ++kt) {
-        ptx::cp_async_wait<STAGES - 2>();
+        ptx::cp_async_wait<CF::STAGES - 2>();
         __syncthreads();
         {
-            const int nk = kt + STAGES - 1;
+            const int nk = kt + CF::STAGES - 1;
             if (nk < KT)
-                load_stage(As + (nk % STAGES) * A_STAGE, Bs + (nk % STAGES) * B_STAGE, A, B, M, N,
-                           K, lda, ldb, m0, n0, (int64_t)nk * BK, tid);
+                load_stage<CF>(As + (nk % CF::STAGES) * CF::A_STAGE, Bs + (nk % CF::STAGES) * CF::B_STAGE, A, B,
+                               M, N, K, lda, ldb, m0, n0, (int64_t)nk * CF::BK, tid);
             ptx::cp_async_commit();
         }
-        const double* as = As + (kt % STAGES) * A_STAGE + (wm * 64) * LDA_S;
-        const double* bs = Bs + (kt % STAGES) * B_STAGE + wn * 32;
+        const double* as = As + (kt % CF::STAGES) * CF::A_STAGE + (wm * CF::TM * 16) * CF::LDA_S;
+        const double* bs = Bs + (kt % CF::STAGES) * CF::B_STAGE + wn * CF::TN * 8;
 #pragma unroll
-        for (int kk = 0; kk < BK; kk += 8) {
-            double af[4][4], bf[4][2];
+        for (int kk = 0; kk < CF::BK; kk += 8) {
+            double af[CF::TM][4], bf[CF::TN][2];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
                 for (int v = 0; v < 4; ++v)
-                    af[i][v] = as[(i * 16 + g + 8 * (v & 1)) * LDA_S + kk + tq + 4 * (v >> 1)];
+                    af[i][v] = as[(i * 16 + g + 8 * (v & 1)) * CF::LDA_S + kk + tq + 4 * (v >> 1)];
 #pragma unroll
-            for (int j = 0; j < 4; ++j)
+            for (int j = 0; j < CF::TN; ++j)
 #pragma unroll
-                for (int v = 0; v < 2; ++v) bf[j][v] = bs[(kk + tq + 4 * v) * LDB_S + j * 8 + g];
+                for (int v = 0; v < 2; ++v) bf[j][v] = bs[(kk + tq + 4 * v) * CF::LDB_S + j * 8 + g];
 #pragma unroll
-            for (int i = 0; i < 4; ++i)
+            for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) dmma_16x8x8(acc[i][j], af[i], bf[j]);
+                for (int j = 0; j < CF::TN; ++j) dmma_16x8x8(acc[i][j], af[i], bf[j]);
         }
     }
     ptx::cp_async_wait<0>();
     // epilogue: c[v] at row g + 8*(v>>1), col 2*tq + (v&1)
 #pragma unroll
-    for (int i = 0; i < 4; ++i)
+    for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < CF::TN; ++j)
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
-                const int64_t r = m0 + wm * 64 + i * 16 + g + 8 * h;
-                const int64_t c = n0 + wn * 32 + j * 8 + 2 * tq;
+                const int64_t r = m0 + wm * CF::TM * 16 + i * 16 + g + 8 * h;
+                const int64_t c = n0 + wn * CF::TN * 8 + j * 8 + 2 * tq;
                 if (r < M) {
                     double* dst = C + r * ldc + c;
                     if (c + 1 < N) {
@@ -167,18 +185,33 @@ inline int64_t kpad(int64_t k) { return (k + 3) / 4 * 4; }  // 16-byte rows for 
 
 // Operand split (G1): hi = rna_tf32(x), lo = rna_tf32(x - hi), both stored as FP32 bit patterns
 // with the low 13 mantissa bits zero.  A: [M][K] -> [M][Kp] (same orientation).
+__device__ __forceinline__ void split1(float x, float& h, float& l) {
+    h = __uint_as_float(ptx::f32_to_tf32_rna(x));
+    l = __uint_as_float(ptx::f32_to_tf32_rna(x - h));
+}
+
+// 2D grid: blockIdx.y = row block, x covers columns in float4 chunks (rows are 16-byte aligned:
+// ldx*4 and ldo*4 are multiples of 16 by the API contract).
 __global__ void split_rows_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
                                   float* __restrict__ hi, float* __restrict__ lo, int64_t ldo) {
-    const int64_t total = rows * cols;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = i / cols, c = i - r * cols;
-        const float x = X[r * ldx + c];
-        const uint32_t h = ptx::f32_to_tf32_rna(x);
-        const float hf = __uint_as_float(h);
-        const uint32_t l = ptx::f32_to_tf32_rna(x - hf);
-        hi[r * ldo + c] = hf;
-        lo[r * ldo + c] = __uint_as_float(l);
+    const int64_t c4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (c4 >= cols) return;
+    for (int64_t r = blockIdx.y; r < rows; r += gridDim.y) {
+        const float* xr = X + r * ldx;
+        float* hr = hi + r * ldo;
+        float* lr = lo + r * ldo;
+        if (c4 + 4 <= cols) {
+            const float4 x = *reinterpret_cast<const float4*>(xr + c4);
+            float4 h, l;
+            split1(x.x, h.x, l.x);
+            split1(x.y, h.y, l.y);
+            split1(x.z, h.z, l.z);
+            split1(x.w, h.w, l.w);
+            *reinterpret_cast<float4*>(hr + c4) = h;
+            *reinterpret_cast<float4*>(lr + c4) = l;
+        } else {
+            for (int64_t c = c4; c < cols; ++c) split1(xr[c], hr[c], lr[c]);
+        }
     }
 }
 
@@ -370,6 +403,176 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     }
 }
 
+// ------------------------------------------------------------ 2-CTA (cta_group::2) kernel
+// A CTA pair computes a 256 x 256 tile: CTA r stages A rows [m0 + 128 r, +128) and B^T rows
+// [n0 + 128 r, +128) (both 128 x 32 fp32 per k-block, hi and lo), so each SM's shared-memory
+// path carries half of each operand (the 1-CTA 128x128 form is bound by the
+// smem data path: TMA writes + operand reads exceed the MMA time).  The leader issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8) into TMEM of both CTAs; each CTA's 8
+// epilogue warps promote their 128 rows x 256 columns (two 128-column halves) into RN FP32
+// registers every KP_BLOCKS k-blocks.
+namespace pair {
+constexpr int BK = 32, STAGES = 3;                         // per-CTA tile halves: 128 x 32
+constexpr int NUM_THREADS = 320;                          // w0 TMA, w1 MMA/TMEM, w2..9 epilogue
+constexpr int NUM_EPI_WARPS = 8;
+constexpr uint32_t TILE_BYTES = 128 * BK * 4;             // 16 KiB
+constexpr uint32_t STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo halves
+constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t ACC_COLS = 256;                        // N of the pair MMA
+constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;              // double-buffered accumulator
+constexpr int KP_BLOCKS = 4;
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+    gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
+                            const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
+                            float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n) {
+    extern __shared__ uint8_t smem_raw[];
+    const uint32_t raw_u32 = ptx::smem_u32(smem_raw);
+    const uint32_t base = (raw_u32 + 1023u) & ~1023u;
+    uint8_t* smem = smem_raw + (base - raw_u32);
+    const uint32_t bar_base = base + STAGES * STAGE_BYTES;
+    auto full_bar = [&](int s) { return bar_base + 8u * s; };
+    auto empty_bar = [&](int s) { return bar_base + 8u * (STAGES + s); };
+    auto tfull_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + b); };
+    auto tempty_bar = [&](int b) { return bar_base + 8u * (2 * STAGES + 2 + b); };
+    const uint32_t tmem_slot = bar_base + 8u * (2 * STAGES + 4);
+    const uint32_t* tmem_slot_ptr =
+        reinterpret_cast<const uint32_t*>(smem + STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4));
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = ptx::cluster_ctarank();
+    const bool leader = rank == 0;
+    int tm, tn;
+    tf32::tile_coords(blockIdx.x >> 1, tiles_m, tiles_n, tm, tn);
+    const int m0 = tm * 256, n0 = tn * 256;
+    const int KB = (K + BK - 1) / BK;
+    const int NCHUNK = (KB + KP_BLOCKS - 1) / KP_BLOCKS;
+
+    if (warp == 0 && lane == 0) {
+        ptx::tma_prefetch_desc(&tmAh);
+        ptx::tma_prefetch_desc(&tmAl);
+        ptx::tma_prefetch_desc(&tmBh);
+        ptx::tma_prefetch_desc(&tmBl);
+        for (int s = 0; s < STAGES; ++s) {
+            ptx::mbar_init(full_bar(s), 1);
+            ptx::mbar_init(empty_bar(s), 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            ptx::mbar_init(tfull_bar(b), 1);
+            ptx::mbar_init(tempty_bar(b), 2 * NUM_EPI_WARPS);  // both CTAs' epilogue warps
+        }
+        ptx::fence_mbar_init();
+    }
+    if (warp == 1) {
+        ptx::tmem_alloc_pair(tmem_slot, TMEM_COLS);
+        ptx::tmem_relinquish_pair();
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    ptx::tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot_ptr;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            // ---------------- TMA producer (both CTAs): own halves, completion on the leader
+            const int am = m0 + 128 * (int)rank, bn = n0 + 128 * (int)rank;
+            for (int kb = 0; kb < KB; ++kb) {
+                const int s = kb % STAGES;
+                const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+                ptx::mbar_wait(empty_bar(s), ph ^ 1u);
+                if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * STAGE_BYTES);
+                const uint32_t st = base + s * STAGE_BYTES;
+                const int kc = kb * BK;
+                ptx::tma_load_2d_pair(st, &tmAh, full_bar(s), kc, am);
+                ptx::tma_load_2d_pair(st + TILE_BYTES, &tmAl, full_bar(s), kc, am);
+                ptx::tma_load_2d_pair(st + 2 * TILE_BYTES, &tmBh, full_bar(s), kc, bn);
+                ptx::tma_load_2d_pair(st + 3 * TILE_BYTES, &tmBl, full_bar(s), kc, bn);
+            }
+        }
+    } else if (warp == 1) {
+        if (leader && lane == 0) {
+            // ---------------- MMA issuer (leader CTA, single thread)
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                                   ((uint32_t)(256 >> 4) << 24);
+            for (int c = 0; c < NCHUNK; ++c) {
+                const int buf = c & 1;
+                ptx::mbar_wait(tempty_bar(buf), ((uint32_t)(c >> 1) & 1u) ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t tmem_d = tmem_base + (uint32_t)(buf * ACC_COLS);
+                const int kb_end = min(KB, (c + 1) * KP_BLOCKS);
+                for (int kb = c * KP_BLOCKS; kb < kb_end; ++kb) {
+                    const int s = kb % STAGES;
+                    const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+                    ptx::mbar_wait(full_bar(s), ph);
+                    ptx::tc_fence_after();
+                    const uint32_t st = base + s * STAGE_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < BK / 8; ++kk) {
+                        const uint32_t off = kk * 32;
+                        const uint64_t ah = ptx::smem_desc_sw128_kmajor(st + off);
+                        const uint64_t al = ptx::smem_desc_sw128_kmajor(st + TILE_BYTES + off);
+                        const uint64_t bh = ptx::smem_desc_sw128_kmajor(st + 2 * TILE_BYTES + off);
+                        const uint64_t bl = ptx::smem_desc_sw128_kmajor(st + 3 * TILE_BYTES + off);
+                        const uint32_t acc0 = (kb > c * KP_BLOCKS || kk > 0) ? 1u : 0u;
+                        ptx::mma_tf32_pair(tmem_d, al, bh, idesc, acc0);
+                        ptx::mma_tf32_pair(tmem_d, ah, bl, idesc, 1u);
+                        ptx::mma_tf32_pair(tmem_d, ah, bh, idesc, 1u);
+                    }
+                    ptx::mma_commit_pair(empty_bar(s), 0x3);  // frees the slot in both CTAs
+                }
+                ptx::mma_commit_pair(tfull_bar(buf), 0x3);    // partial sum ready in both CTAs
+            }
+        }
+    } else {
+        // ---------------- epilogue warps 2..9: lanes 32*(warp%4), column half (warp-2)/4
+        const int q = warp & 3;
+        const int h = (warp - 2) >> 2;
+        float acc[128];
+#pragma unroll
+        for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+        for (int c = 0; c < NCHUNK; ++c) {
+            const int buf = c & 1;
+            ptx::mbar_wait(tfull_bar(buf), (uint32_t)(c >> 1) & 1u);
+            ptx::tc_fence_after();
+            const uint32_t taddr =
+                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC_COLS + h * 128);
+#pragma unroll
+            for (int cb = 0; cb < 128; cb += 32) {
+                uint32_t r[32];
+                ptx::tmem_ld_32x32b_x32(taddr + (uint32_t)cb, r);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 32; ++j) acc[cb + j] += __uint_as_float(r[j]);
+            }
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive_leader(tempty_bar(buf));
+        }
+        const int row = m0 + 128 * (int)rank + q * 32 + lane;
+        const int col0 = n0 + h * 128;
+        if (row < M) {
+            float* dst = C + (int64_t)row * ldc + col0;
+            const int valid = N - col0;
+            if (valid >= 128) {
+#pragma unroll
+                for (int j = 0; j < 128; j += 4)
+                    *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 128; ++j)
+                    if (j < valid) dst[j] = acc[j];
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_sync();
+    if (warp == 1) {
+        ptx::tc_fence_after();
+        ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    }
+}
+}  // namespace pair
+
 // ------------------------------------------------------------ host: TMA descriptors
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
@@ -412,6 +615,27 @@ static fb_status make_kmajor_map(CUtensorMap* map, const float* ptr, int64_t row
 }
 }  // namespace tf32
 
+template <class CF>
+static fb_status launch_f64(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                            void* C, int64_t ldc, cudaStream_t s) {
+    auto kern = f64::gemm_f64_dmma_kernel<CF>;
+    static int attr_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_mask & (1 << (dev & 31)))) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+        attr_mask |= 1 << (dev & 31);
+    }
+    dim3 grid((unsigned)((n + CF::BN - 1) / CF::BN), (unsigned)((m + CF::BM - 1) / CF::BM));
+    if (grid.y > 65535) {
+        set_error("m too large for the FP64 grid");
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    kern<<<grid, CF::THREADS, CF::SMEM, s>>>((const double*)A, (const double*)B, (double*)C, m, n, k, lda, ldb, ldc);
+    FB_LAUNCH_CHECK("gemm_f64_dmma_kernel");
+    return FB_OK;
+}
+
 size_t gemm_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
     if (dtype == FB_F64) return 0;
     const int64_t kp = tf32::kpad(k);
@@ -422,23 +646,11 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
                       const void* B, int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
                       const DeviceState* st, cudaStream_t s) {
     if (dtype == FB_F64) {
-        static int attr_mask = 0;
-        int dev = 0;
-        cudaGetDevice(&dev);
-        if (!(attr_mask & (1 << (dev & 31)))) {
-            FB_CUDA_TRY(cudaFuncSetAttribute(f64::gemm_f64_dmma_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)f64::SMEM));
-            attr_mask |= 1 << (dev & 31);
-        }
-        dim3 grid((unsigned)((n + f64::BN - 1) / f64::BN), (unsigned)((m + f64::BM - 1) / f64::BM));
-        if (grid.y > 65535) {
-            set_error("m too large for the FP64 grid");
-            return FB_ERR_UNSUPPORTED_SIZE;
-        }
-        f64::gemm_f64_dmma_kernel<<<grid, f64::THREADS, f64::SMEM, s>>>(
-            (const double*)A, (const double*)B, (double*)C, m, n, k, lda, ldb, ldc);
-        FB_LAUNCH_CHECK("gemm_f64_dmma_kernel");
-        return FB_OK;
+        const char* kv = getenv("FB_F64_CFG");  // A/B knob: 0 = 64x64 (default), 1 = 128x128, 2 = 128x64
+        const int cfg = kv ? atoi(kv) : 0;
+        if (cfg == 1) return launch_f64<f64::Cfg<128, 128, 2, 4>>(m, n, k, A, lda, B, ldb, C, ldc, s);
+        if (cfg == 2) return launch_f64<f64::Cfg<128, 64, 2, 2>>(m, n, k, A, lda, B, ldb, C, ldc, s);
+        return launch_f64<f64::CfgSmall>(m, n, k, A, lda, B, ldb, C, ldc, s);
     }
     // ---- FP32 via 3xTF32: split A (same orientation), split B transposed, then the MMA kernel
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) {
@@ -462,12 +674,9 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
 fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
                             float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s) {
     if (!transpose) {
-        const int64_t total = rows * cols;
-        int64_t blocks = (total + 255) / 256;
-        const int64_t cap = (int64_t)st->sm_count * 16;
-        if (blocks > cap) blocks = cap;
-        if (blocks < 1) blocks = 1;
-        tf32::split_rows_kernel<<<(unsigned)blocks, 256, 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
+        const int64_t chunks = (cols + 3) / 4;
+        dim3 g((unsigned)((chunks + 127) / 128), (unsigned)(rows < 8192 ? rows : 8192));
+        tf32::split_rows_kernel<<<g, 128, 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
         FB_LAUNCH_CHECK("split_rows_kernel");
     } else {
         dim3 g2((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
@@ -492,10 +701,27 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
     static int attr_mask = 0;
     int dev = 0;
     cudaGetDevice(&dev);
+    const char* knob = getenv("FB_GEMM_1CTA");
+    const bool one_cta = knob && knob[0] == '1';
     if (!(attr_mask & (1 << (dev & 31)))) {
         FB_CUDA_TRY(cudaFuncSetAttribute(tf32::gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tf32::SMEM));
+        FB_CUDA_TRY(cudaFuncSetAttribute(tf32::pair::gemm_3xtf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)tf32::pair::SMEM));
         attr_mask |= 1 << (dev & 31);
+    }
+    if (!one_cta) {
+        const int tiles_m = (int)((m + 255) / 256);
+        const int tiles_n = (int)((n + 255) / 256);
+        const int64_t tiles = (int64_t)tiles_m * tiles_n;
+        if (2 * tiles > INT32_MAX) {
+            set_error("too many tiles");
+            return FB_ERR_UNSUPPORTED_SIZE;
+        }
+        tf32::pair::gemm_3xtf32_pair_kernel<<<(unsigned)(2 * tiles), tf32::pair::NUM_THREADS, tf32::pair::SMEM, s>>>(
+            mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, ldc, tiles_m, tiles_n);
+        FB_LAUNCH_CHECK("gemm_3xtf32_pair_kernel");
+        return FB_OK;
     }
     const int tiles_m = (int)((m + tf32::BM - 1) / tf32::BM);
     const int tiles_n = (int)((n + tf32::BN - 1) / tf32::BN);
