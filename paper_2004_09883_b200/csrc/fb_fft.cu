@@ -254,6 +254,8 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
 
     const float2* src = p.in + gh * p.lin.hi + gl * p.lin.lo;
     float2* dst = p.out + gh * p.lout.hi + gl * p.lout.lo;
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();  // PDL: the previous pass's output is complete and visible
 
     float2 v[G::E];
     if constexpr (MODE == 1) {
@@ -329,6 +331,33 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
     }
 }
 
+// Tuning knobs read once from the environment (for A/B measurements; defaults are the tuned
+// configuration).
+static int fft_knob(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+static bool fft_pdl_enabled() { return fft_knob("FB_FFT_NO_PDL", 0) == 0; }
+
+// Launch with programmatic stream serialization: the kernel may start while the previous
+// kernel on the stream drains; every FFT kernel calls pdl_wait() before touching global memory.
+template <typename Kern, typename... Args>
+static fb_status launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = fft_pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+    FB_LAUNCH_CHECK("fft pass");
+    return FB_OK;
+}
+
 template <int LOG2L, int C, int MODE>
 static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     using G = LineGeom<LOG2L>;
@@ -348,8 +377,8 @@ static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_
         set_error("FFT pass grid too large (%lld CTAs)", (long long)blocks);
         return FB_ERR_UNSUPPORTED_SIZE;
     }
-    fft_pass_kernel<LOG2L, C, MODE><<<(unsigned)blocks, threads, smem, s>>>(p, st->twiddles, st->stage_tw);
-    FB_LAUNCH_CHECK("fft_pass_kernel");
+    FB_TRY(launch_pdl(fft_pass_kernel<LOG2L, C, MODE>, dim3((unsigned)blocks), dim3(threads), smem, s, p,
+                      (const float2*)st->twiddles, (const float2*)st->stage_tw));
     return FB_OK;
 }
 
@@ -450,6 +479,8 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, 1)
         }
     }
     __syncthreads();
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();  // PDL: everything above overlapped the previous grid's tail
 
     // thread 0: start the asynchronous fill of staging buffer `buf` with group `grp`
     auto issue = [&](int64_t grp, int buf) {
@@ -642,17 +673,11 @@ static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStr
             return FB_ERR_CUDA;
         }
     }
-    kern<<<(unsigned)grid, threads, TG::SMEM, s>>>(p, tin, tout, st->twiddles, st->stage_tw, ngroups, nh);
-    FB_LAUNCH_CHECK("fft_pass_tma_kernel");
+    FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), TG::SMEM, s, p, tin, tout,
+                      (const float2*)st->twiddles, (const float2*)st->stage_tw, ngroups, nh));
     return FB_OK;
 }
 
-// Tuning knobs read once from the environment (for A/B measurements; defaults are the tuned
-// configuration).
-static int fft_knob(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return (e && e[0]) ? atoi(e) : dflt;
-}
 
 // Picks the TMA path when the pass is expressible; returns false to fall back.
 static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic) {

@@ -1,9 +1,10 @@
 cd $GRAFT_REPO_ROOT
 rm -f gpurun_out/ab.jsonl
-for shp in "2048 2048" "16384 16384" "256 256" "8192 2048"; do
+timeout 400 python -m pytest tests/test_fft_gpu.py tests/test_comm_gpu.py -m gpu -q -x 2>&1 | tail -1 > gpurun_out/ab_tests.log
+for shp in "2048 2048" "256 256" "16384 16384"; do
   set -- $shp
-  FLUSH=write+read timeout 60 python tools/fft_pass_bench.py $1 $2 20 >> gpurun_out/ab.jsonl 2>&1
-  FLUSH=write+read FB_FFT_NO_TMA_COL=1 timeout 60 python tools/fft_pass_bench.py $1 $2 20 >> gpurun_out/ab.jsonl 2>&1
+  timeout 60 python tools/fft_pass_bench.py $1 $2 20 >> gpurun_out/ab.jsonl 2>&1
+  FB_FFT_NO_PDL=1 timeout 60 python tools/fft_pass_bench.py $1 $2 20 >> gpurun_out/ab.jsonl 2>&1
 done
-FLUSH=write+read FB_FFT_COL_C=4 timeout 60 python tools/fft_pass_bench.py 2048 2048 20 >> gpurun_out/ab.jsonl 2>&1
-FLUSH=write+read FB_FFT_COL_C=8 timeout 60 python tools/fft_pass_bench.py 16384 16384 10 >> gpurun_out/ab.jsonl 2>&1
+timeout 200 python bench.py --steps 20 --warmup 5 --no-extras > gpurun_out/b_pdl.json 2>&1
+FB_FFT_NO_PDL=1 timeout 200 python bench.py --steps 20 --warmup 5 --no-extras > gpurun_out/b_nopdl.json 2>&1
