@@ -165,13 +165,35 @@ void stage_tw_index(int32_t* idx) {
         }
 }
 
+// Twiddles of stage S for this thread's butterflies j = t + q T: tw[q][r-1] = W_{Ns R}^{(j mod Ns) r}.
+template <int LOG2L, int S>
+struct StageTw {
+    static constexpr int R = stage_radix(LOG2L, S);
+    static constexpr int Q = LineGeom<LOG2L>::E / R;
+    static constexpr int NT = (S == 0) ? 1 : Q * (R - 1);
+    __device__ __forceinline__ static void load(float2* tw, int t, const float2* __restrict__ stw) {
+        if constexpr (S > 0) {
+            constexpr int Ns = 1 << (4 * S);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int jm = (t + q * LineGeom<LOG2L>::T) & (Ns - 1);
+                const float2* twp = stw + stage_tw_offset(LOG2L, S) + jm;
+#pragma unroll
+                for (int r = 1; r < R; ++r) tw[q * (R - 1) + r - 1] = __ldg(twp + r * Ns);
+            }
+        }
+    }
+};
+
 // Stage `S` (0-based): radix R, Ns = 16^S.  v[m] holds element t + m T of the stage input
-// on entry (stage 0: loaded from global by the caller) and of the stage output on exit.
+// on entry (stage 0: loaded by the caller) and of the stage output on exit.  `tw` holds this
+// stage's twiddles, prefetched by the previous stage just before its barrier (the element
+// registers are dead there, so the loads overlap the barrier and the exchange reads).
 template <int LOG2L, int C, int S>
 struct Stages {
     using G = LineGeom<LOG2L>;
     __device__ __forceinline__ static void run(float2* v, float2* sm, int t, int c,
-                                               const float2* __restrict__ stw) {
+                                               const float2* __restrict__ stw, const float2* tw) {
         if constexpr (S < G::NSTAGES) {
             constexpr int R = stage_radix(LOG2L, S);
             constexpr int Ns = 1 << (4 * S);
@@ -197,11 +219,8 @@ struct Stages {
 #pragma unroll
                 for (int r = 0; r < R; ++r) b[r] = v[q + r * Q];
                 if constexpr (!first) {
-                    // table layout [r][jm]: lanes with consecutive jm read consecutive entries
-                    const int jm = (t + q * T) & (Ns - 1);
-                    const float2* twp = stw + stage_tw_offset(LOG2L, S) + jm;
 #pragma unroll
-                    for (int r = 1; r < R; ++r) b[r] = cmul(b[r], __ldg(twp + r * Ns));
+                    for (int r = 1; r < R; ++r) b[r] = cmul(b[r], tw[q * (R - 1) + r - 1]);
                 }
                 dft<R>(b);
 #pragma unroll
@@ -221,17 +240,15 @@ struct Stages {
 #pragma unroll
                     for (int r = 0; r < R; ++r) wp[r * (Ns + Ns / 16) * C] = v[r];
                 }
+                float2 twn[StageTw<LOG2L, S + 1>::NT];
+                StageTw<LOG2L, S + 1>::load(twn, t, stw);
                 __syncthreads();
-                Stages<LOG2L, C, S + 1>::run(v, sm, t, c, stw);
+                Stages<LOG2L, C, S + 1>::run(v, sm, t, c, stw, twn);
             }
         }
     }
 };
 
-// MODE (addressing of the global loads/stores):
-//   1: both maps unblocked with unit element stride (rows): compile-time offsets;
-//   2: both maps unblocked, strided elements (columns): pointer increments;
-//   0: general LineMap (per-peer blocks of the slab all-to-all).
 #ifndef FB_FFT_THREADS_PER_SM
 #define FB_FFT_THREADS_PER_SM 1024  // occupancy target -> register cap 65536 / this
 #endif
@@ -284,7 +301,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
         for (int m = 0; m < G::E; ++m) v[m].y = -v[m].y;
     }
 
-    Stages<LOG2L, C, 0>::run(v, sm, t, c, stw);
+    Stages<LOG2L, C, 0>::run(v, sm, t, c, stw, nullptr);
 
     if (!valid) return;
     if (p.tw4_log2N > 0) {
@@ -547,7 +564,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, 1)
             if (nxt < ngroups) issue(nxt, buf);
         }
 
-        Stages<LOG2L, C, 0>::run(v, X, t, c, stw);
+        Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
 
         const int64_t g = grp * C + c;
         const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
@@ -787,14 +804,16 @@ static LineMap plain_map(int64_t hi, int64_t lo, int64_t es) {
     return m;
 }
 
-static constexpr int kMaxOnChipCol = 12;  // column lines up to 4096 in one pass
+// column lines up to 2^12 in one pass (knob FB_FFT_COL_MAX_LOG2 for A/B; longer ones use the
+// four-step split)
+static int max_onchip_col() { return fft_knob("FB_FFT_COL_MAX_LOG2", 12); }
 
 fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, int64_t ld_in,
                       int64_t ld_out, bool conj_in, bool conj_out, float scale, float2* tmp,
                       const DeviceState* st, cudaStream_t s) {
     const int l0 = ilog2(n0);
     const int lc = ilog2(ncols);
-    if (l0 <= kMaxOnChipCol) {
+    if (l0 <= max_onchip_col()) {
         FftPass p{};
         p.in = in;
         p.out = out;
@@ -818,7 +837,7 @@ fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, 
         set_error("internal: four-step column FFT needs a workspace");
         return FB_ERR_WORKSPACE;
     }
-    const int lb = 7;
+    const int lb = fft_knob("FB_FFT_4STEP_LB", l0 >= 14 ? 7 : (l0 + 1) / 2);
     const int la = l0 - lb;
     const int64_t a = int64_t(1) << la, b = int64_t(1) << lb;
     FftPass p1{};
@@ -852,14 +871,14 @@ fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, 
 }
 
 size_t fft2d_ws_bytes(int64_t n0, int64_t n1) {
-    if (ilog2(n0) <= kMaxOnChipCol) return 0;
+    if (ilog2(n0) <= max_onchip_col()) return 0;
     return (size_t)n0 * (size_t)n1 * sizeof(float2);
 }
 
 fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
                        size_t ws_bytes, const DeviceState* st, cudaStream_t s) {
     const float scale = inverse ? 1.0f / (float)((double)n0 * (double)n1) : 1.0f;
-    const bool four_step = ilog2(n0) > kMaxOnChipCol;
+    const bool four_step = ilog2(n0) > max_onchip_col();
     float2* rowout = four_step ? (float2*)ws : (float2*)y;
     if (four_step && ws_bytes < fft2d_ws_bytes(n0, n1)) {
         set_error("workspace too small");
