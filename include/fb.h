@@ -130,6 +130,19 @@ fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void*
                          const void* B_host, void* C_host, void* dev, size_t dev_bytes,
                          void* stream);
 
+/* NR-compatible shim (the paper's C-1/C-2 interface matching, for the
+ * Numerical Recipes in C applications it offloads): the argument list of NR's
+ *     void fourn(float data[], unsigned long nn[], int ndim, int isign)
+ * so a rewritten call site needs no other change.  NR conventions: 1-based arrays (data[1] is
+ * the real part of the first element, nn[1..ndim] are the sizes, nn[1] the slowest index),
+ * complex interleaved, isign = +1 computes sum x exp(+2 pi i k.n/N) and isign = -1 the
+ * exp(-2 pi i ...) transform, both UNSCALED, in place on the host array.  ndim is 1 or 2;
+ * sizes powers of two <= 16384.  Host data is copied to the GPU, transformed with the same
+ * kernels as fb_fft2d, and copied back (the transfers the paper counts); the shim owns
+ * a cached device staging buffer (it has no way to receive one) and synchronises the host.
+ * Returns an fb_status (NR's fourn returns void; callers that ignore it keep NR semantics). */
+fb_status fb_nr_fourn(float data[], const unsigned long nn[], int ndim, int isign);
+
 /* ------------------------------------------------------------------ multi-GPU
  * One process per GPU.  Rank 0 calls fb_comm_unique_id and the caller distributes the
  * 128 bytes (e.g. torch.distributed broadcast); every rank then calls fb_comm_init.

@@ -32,7 +32,7 @@ EXPORTS = [
     "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
     "fb_comm_size", "fb_fft2d_slab_workspace_bytes", "fb_fft2d_slab", "fb_ifft2d_slab",
-    "fb_matmul_rowblock_workspace_bytes", "fb_matmul_rowblock",
+    "fb_matmul_rowblock_workspace_bytes", "fb_matmul_rowblock", "fb_nr_fourn",
 ]
 
 
@@ -82,6 +82,7 @@ def lib() -> ctypes.CDLL:
         "fb_ifft2d_slab": ([vp, vp, vp, i64, i64, vp, sz, vp], ci),
         "fb_matmul_rowblock_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
         "fb_matmul_rowblock": ([vp, ci, i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, vp, sz, vp], ci),
+        "fb_nr_fourn": ([vp, vp, ci, ci], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -246,6 +247,16 @@ def fb_matmul_host(A_host: torch.Tensor, B_host: torch.Tensor, C_host: torch.Ten
     dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
     _check("fb_matmul_host", lib().fb_matmul_host(dt, m, n, k, _ptr(A_host), _ptr(B_host), _ptr(C_host),
                                                   _ptr(dev), dev.numel(), _stream(stream)))
+
+
+def fb_nr_fourn(data, nn, ndim: int, isign: int):
+    """NR fourn(data, nn, ndim, isign) on host numpy arrays with NR's 1-based layout:
+    data is float32 of length 2*prod(nn)+1 (data[0] unused), nn is uint64 of length ndim+1."""
+    import numpy as np
+    if data.dtype != np.float32 or not data.flags.c_contiguous:
+        raise ValueError("data must be a contiguous float32 array (NR 1-based)")
+    nn = np.ascontiguousarray(nn, dtype=np.uint64)
+    _check("fb_nr_fourn", lib().fb_nr_fourn(data.ctypes.data, nn.ctypes.data, ndim, isign))
 
 
 # ------------------------------------------------------------------ multi-GPU

@@ -373,4 +373,40 @@ fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void*
     return FB_OK;
 }
 
+// ---------------------------------------------------------------- NR-compatible shim (N3)
+fb_status fb_nr_fourn(float data[], const unsigned long nn[], int ndim, int isign) {
+    clear_error();
+    if (!data || !nn || (ndim != 1 && ndim != 2) || (isign != 1 && isign != -1)) {
+        set_error("fb_nr_fourn: need data, nn, ndim in {1,2}, isign = +-1");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const int64_t n0 = ndim == 2 ? (int64_t)nn[1] : 1;
+    const int64_t n1 = ndim == 2 ? (int64_t)nn[2] : (int64_t)nn[1];
+    FB_TRY(check_fft_dims(n0, n1));
+    DeviceState* st;
+    int dev = 0;
+    FB_TRY(ensure_device(&dev, &st));
+    static std::mutex mu;
+    static void* buf[kMaxDev] = {nullptr};
+    static size_t cap[kMaxDev] = {0};
+    std::lock_guard<std::mutex> lk(mu);
+    const size_t bytes = (size_t)n0 * n1 * sizeof(float2);
+    const size_t need = round_up(bytes, 256) + fft2d_ws_bytes(n0, n1);
+    if (cap[dev] < need) {
+        if (buf[dev]) cudaFree(buf[dev]);
+        buf[dev] = nullptr;
+        cap[dev] = 0;
+        FB_CUDA_TRY(cudaMalloc(&buf[dev], need));
+        cap[dev] = need;
+    }
+    char* d = (char*)buf[dev];
+    void* ws = d + round_up(bytes, 256);
+    float* host = data + 1;  // NR 1-based: data[1] is the first real part
+    // NR isign = -1 is our forward (exp(-2 pi i)); isign = +1 our inverse, left unscaled
+    FB_CUDA_TRY(cudaMemcpy(d, host, bytes, cudaMemcpyHostToDevice));
+    FB_TRY(fft2d_device(d, d, n0, n1, isign == 1, ws, fft2d_ws_bytes(n0, n1), st, 0, /*unscaled=*/true));
+    FB_CUDA_TRY(cudaMemcpy(host, d, bytes, cudaMemcpyDeviceToHost));
+    return FB_OK;
+}
+
 }  // extern "C"

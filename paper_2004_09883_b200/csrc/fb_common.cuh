@@ -104,7 +104,7 @@ fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t 
 // Full single-GPU 2D FFT on device buffers (used by the API and the host/slab variants).
 size_t fft2d_ws_bytes(int64_t n0, int64_t n1);
 fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
-                       size_t ws_bytes, const DeviceState* st, cudaStream_t s);
+                       size_t ws_bytes, const DeviceState* st, cudaStream_t s, bool unscaled = false);
 // Column transform of an n0 x ncols block with leading dimension ld (in place allowed when
 // n0 <= 4096); used by 2D and slab paths.
 fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, int64_t ld_in,

@@ -876,8 +876,8 @@ size_t fft2d_ws_bytes(int64_t n0, int64_t n1) {
 }
 
 fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
-                       size_t ws_bytes, const DeviceState* st, cudaStream_t s) {
-    const float scale = inverse ? 1.0f / (float)((double)n0 * (double)n1) : 1.0f;
+                       size_t ws_bytes, const DeviceState* st, cudaStream_t s, bool unscaled) {
+    const float scale = (inverse && !unscaled) ? 1.0f / (float)((double)n0 * (double)n1) : 1.0f;
     const bool four_step = ilog2(n0) > max_onchip_col();
     float2* rowout = four_step ? (float2*)ws : (float2*)y;
     if (four_step && ws_bytes < fft2d_ws_bytes(n0, n1)) {

@@ -71,6 +71,14 @@ def test_matmul_validation_without_device(L):
     assert L.fb_matmul_workspace_bytes(0, 64, 32, 30) == (2 * 64 * 32 + 2 * 32 * 32) * 4
 
 
+def test_nr_shim_validation_without_device(L):
+    nn = (ctypes.c_ulong * 3)(0, 3, 4)
+    data = (ctypes.c_float * 25)()
+    assert L.fb_nr_fourn(data, nn, 2, -1) == 2   # 3 is not a power of two
+    assert L.fb_nr_fourn(data, nn, 3, -1) == 1   # ndim 3 unsupported
+    assert L.fb_nr_fourn(data, nn, 2, 0) == 1    # isign must be +-1
+
+
 def test_comm_validation_without_device(L):
     assert L.fb_comm_unique_id_bytes() == 128
     p = ctypes.c_void_p(16)

@@ -178,3 +178,23 @@ def test_host_variant(fb):
     assert oracle.rel_l2(yh.numpy(), oracle.dft2d(x)) < 5e-7
     fb.fb_fft2d_host(yh, xh, inverse=True)
     assert oracle.rel_l2(xh.numpy(), x) < 5e-7
+
+
+@pytest.mark.parametrize("n0,n1", [(64, 128), (1, 256), (256, 256)])
+def test_nr_fourn_shim(fb, n0, n1):
+    """NR fourn conventions: 1-based data/nn, isign=-1 -> exp(-2 pi i), isign=+1 ->
+    exp(+2 pi i), both unscaled, in place on the host array."""
+    x = synth.complex_field(n0, n1)
+    data = np.zeros(2 * n0 * n1 + 1, dtype=np.float32)
+    data[1:] = x.view(np.float32).ravel()
+    if n0 == 1:
+        nn, ndim = np.array([0, n1], dtype=np.uint64), 1
+    else:
+        nn, ndim = np.array([0, n0, n1], dtype=np.uint64), 2
+    fb.fb_nr_fourn(data, nn, ndim, -1)
+    y = data[1:].view(np.complex64).reshape(n0, n1)
+    assert oracle.rel_l2(y, oracle.dft2d(x)) < 5e-7
+    fb.fb_nr_fourn(data, nn, ndim, +1)   # unscaled inverse: returns N * x
+    z = data[1:].view(np.complex64).reshape(n0, n1)
+    assert oracle.rel_l2(z, (n0 * n1) * x.astype(np.complex128)) < 5e-7
+    assert data[0] == 0.0  # the unused NR slot is untouched
