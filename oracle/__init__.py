@@ -46,9 +46,10 @@ def lib():
         L.oracle_matmul_rows.argtypes = [i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, dp, ci]
         L.oracle_matmul_cols.argtypes = [i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, dp, ci]
         L.oracle_threads.argtypes = [ci]
+        L.oracle_lu.argtypes = [i64, vp, i64, vp, ci]
         for f in ("oracle_dft2d", "oracle_dft2d_bruteforce", "oracle_dft2d_col",
                   "oracle_dft2d_row", "oracle_matmul", "oracle_matmul_rows",
-                  "oracle_matmul_cols", "oracle_threads"):
+                  "oracle_matmul_cols", "oracle_threads", "oracle_lu"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -171,3 +172,24 @@ def rel_l2(y, ref) -> float:
     den = np.linalg.norm(ref.ravel())
     num = np.linalg.norm((y - ref).ravel())
     return float(num / den) if den > 0 else float(num)
+
+
+def lu(A, nthreads: int = 0):
+    """P A = L U with partial pivoting (P:153/P:165 LU block). Returns (LU, ipiv, info):
+    LU holds unit-lower L below the diagonal and U on/above it; ipiv[k] = row swapped with k."""
+    LU = np.array(A, dtype=np.float64, order="C", copy=True)
+    n = LU.shape[0]
+    assert LU.shape == (n, n)
+    ipiv = np.empty(n, dtype=np.int32)
+    info = lib().oracle_lu(n, LU.ctypes.data, n, ipiv.ctypes.data, nthreads)
+    if info < 0:
+        raise RuntimeError("oracle_lu failed")
+    return LU, ipiv, info
+
+
+def lu_permutation(ipiv) -> np.ndarray:
+    """Row order p such that (P A)[i] = A[p[i]] for the swap sequence ipiv."""
+    p = np.arange(len(ipiv))
+    for k, q in enumerate(ipiv):
+        p[k], p[q] = p[q], p[k]
+    return p

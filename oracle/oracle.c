@@ -301,3 +301,39 @@ int oracle_matmul_cols(int64_t m, int64_t n, int64_t k, const void* A, int64_t l
     }
     return 0;
 }
+
+int oracle_lu(int64_t n, double* A, int64_t lda, int32_t* ipiv, int threads) {
+    if (n < 0 || lda < n) return -1;
+    int nt = oracle_threads(threads);
+    (void)nt;
+    int info = 0;
+    for (int64_t k = 0; k < n; ++k) {
+        /* pivot: first row with the largest magnitude in column k */
+        int64_t p = k;
+        double best = fabs(A[k * lda + k]);
+        for (int64_t i = k + 1; i < n; ++i) {
+            double v = fabs(A[i * lda + k]);
+            if (v > best) { best = v; p = i; }
+        }
+        ipiv[k] = (int32_t)p;
+        if (p != k)
+            for (int64_t j = 0; j < n; ++j) {
+                double t = A[k * lda + j];
+                A[k * lda + j] = A[p * lda + j];
+                A[p * lda + j] = t;
+            }
+        double piv = A[k * lda + k];
+        if (piv == 0.0) {
+            if (!info) info = (int)(k + 1);
+            continue;
+        }
+        /* multipliers, then the rank-1 update of the trailing matrix */
+#pragma omp parallel for num_threads(nt) schedule(static)
+        for (int64_t i = k + 1; i < n; ++i) {
+            double l = A[i * lda + k] / piv;
+            A[i * lda + k] = l;
+            for (int64_t j = k + 1; j < n; ++j) A[i * lda + j] -= l * A[k * lda + j];
+        }
+    }
+    return info;
+}
