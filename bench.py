@@ -371,6 +371,27 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                          "peak": f64_peak, "unit": "TFLOP/s", "frac": flops / (t * 1e-3) / 1e12 / f64_peak,
                          "peak_source": "DMMA pipe peak derived from ncu utilisation (37.1 TFLOP/s)"}}
         del A, B, C
+    # the paper's own matrix workload, LU of a 2048x2048 orthogonal matrix
+    if want("lu_f64_2048"):
+        n = 2048
+        Q = torch.from_numpy(synth.dct2_matrix(n)).cuda()
+        LUb = torch.empty_like(Q)
+        ipiv = torch.empty(n, dtype=torch.int32, device="cuda")
+        info = torch.zeros(1, dtype=torch.int32, device="cuda")
+
+        def restore_and_flush():  # untimed: the factorisation is in place
+            LUb.copy_(Q)
+            flush()
+        ms = timed_steps(torch, lambda: fb.fb_lu(LUb, ipiv, info, stream), steps, args.warmup, restore_and_flush,
+                         stream)
+        t = float(np.mean(ms))
+        flops = 2.0 / 3.0 * n ** 3
+        res["lu_f64_2048"] = {"value": flops / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
+                              "config": {"workload": "lu_2048_fp64_orthogonal_dct2", "survey_next": "N2",
+                                         "flops": "2/3 n^3"},
+                              "note": "8-column register-resident panels + DMMA trailing updates; "
+                                      "latency-bound by the 2048 sequential pivot steps"}
+        del Q, LUb
     # configs[0]: 256^2 forward + inverse
     if want("fft2d_256_fwd_inv"):
         m = 256

@@ -130,6 +130,19 @@ fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void*
                          const void* B_host, void* C_host, void* dev, size_t dev_bytes,
                          void* stream);
 
+/* ------------------------------------------------------------------ LU block
+ * The paper's actual matrix workload: "LU decomposition processing of 2048*2048 orthogonal
+ * matrix data", replaced there by cuSOLVER getrf; reading R19.
+ * P A = L U in place on the row-major n x n matrix A (device, leading dim lda, 16-byte
+ * aligned, lda even): L unit lower (strictly below the diagonal), U upper.  LAPACK getrf
+ * pivoting: at step k the pivot is the FIRST row p >= k of largest |A[p][k]|; whole rows are
+ * swapped; ipiv[k] = p (device int32[n], 0-based).  *info (device int32) = 0, or k+1 for the
+ * first exactly-zero pivot (that step is skipped, as LAPACK).  dtype FB_F64 only; n <= 4096.
+ * ws: fb_lu_workspace_bytes(dtype, n) bytes (currently 0). */
+size_t fb_lu_workspace_bytes(int dtype, int64_t n);
+fb_status fb_lu(int dtype, int64_t n, void* A, int64_t lda, int32_t* ipiv, int32_t* info, void* ws,
+                size_t ws_bytes, void* stream);
+
 /* NR-compatible shim (the paper's C-1/C-2 interface matching, for the
  * Numerical Recipes in C applications it offloads): the argument list of NR's
  *     void fourn(float data[], unsigned long nn[], int ndim, int isign)

@@ -33,6 +33,7 @@ EXPORTS = [
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
     "fb_comm_size", "fb_fft2d_slab_workspace_bytes", "fb_fft2d_slab", "fb_ifft2d_slab",
     "fb_matmul_rowblock_workspace_bytes", "fb_matmul_rowblock", "fb_nr_fourn",
+    "fb_lu_workspace_bytes", "fb_lu",
 ]
 
 
@@ -83,6 +84,8 @@ def lib() -> ctypes.CDLL:
         "fb_matmul_rowblock_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
         "fb_matmul_rowblock": ([vp, ci, i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, vp, sz, vp], ci),
         "fb_nr_fourn": ([vp, vp, ci, ci], ci),
+        "fb_lu_workspace_bytes": ([ci, i64], sz),
+        "fb_lu": ([ci, i64, vp, i64, vp, vp, vp, sz, vp], ci),
     }
     for name, (args, res) in sig.items():
         f = getattr(L, name)
@@ -247,6 +250,28 @@ def fb_matmul_host(A_host: torch.Tensor, B_host: torch.Tensor, C_host: torch.Ten
     dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
     _check("fb_matmul_host", lib().fb_matmul_host(dt, m, n, k, _ptr(A_host), _ptr(B_host), _ptr(C_host),
                                                   _ptr(dev), dev.numel(), _stream(stream)))
+
+
+def fb_lu(A: torch.Tensor, ipiv: torch.Tensor, info: torch.Tensor, stream=None):
+    """P A = L U in place (FP64, row-major, LAPACK getrf pivoting; ipiv int32 0-based)."""
+    n = A.shape[0]
+    _check("fb_lu", lib().fb_lu(FB_F64, n, _ptr(A), A.stride(0), _ptr(ipiv), _ptr(info), None, 0,
+                                _stream(stream)))
+
+
+def lu(A: torch.Tensor, stream=None):
+    """Returns (LU, ipiv, info) for a square float64 CUDA tensor (A is not modified)."""
+    if A.dtype != torch.float64 or A.dim() != 2 or A.shape[0] != A.shape[1]:
+        raise ValueError("lu expects a square float64 CUDA tensor")
+    n = A.shape[0]
+    ldp = n + (n & 1)  # the C ABI needs an even leading dimension (16-byte rows for DMMA loads)
+    buf = torch.zeros(n, ldp, dtype=A.dtype, device=A.device)
+    buf[:, :n].copy_(A)
+    LU = buf[:, :n]
+    ipiv = torch.empty(A.shape[0], dtype=torch.int32, device=A.device)
+    info = torch.zeros(1, dtype=torch.int32, device=A.device)
+    fb_lu(LU, ipiv, info, stream)
+    return LU, ipiv, info
 
 
 def fb_nr_fourn(data, nn, ndim: int, isign: int):

@@ -85,10 +85,11 @@ __device__ __forceinline__ void load_stage(double* As, double* Bs, const double*
 
 // The k-loop order (k-blocks ascending, then kk, then the DMMA's internal order) is the same
 // for every tile shape, so results are bitwise identical across configurations.
-template <class CF>
+// SUB: C <- C - A B (the LU trailing update), else C <- A B.
+template <class CF, bool SUB = false>
 __global__ void __launch_bounds__(CF::THREADS)
     gemm_f64_dmma_kernel(const double* __restrict__ A, const double* __restrict__ B,
-                         double* __restrict__ C, int64_t M, int64_t N, int64_t K, int64_t lda,
+                         double* C, int64_t M, int64_t N, int64_t K, int64_t lda,
                          int64_t ldb, int64_t ldc) {
     extern __shared__ __align__(128) double smem_d[];
     double* As = smem_d;
@@ -157,9 +158,14 @@ __global__ void __launch_bounds__(CF::THREADS)
                 if (r < M) {
                     double* dst = C + r * ldc + c;
                     if (c + 1 < N) {
-                        *reinterpret_cast<double2*>(dst) = make_double2(acc[i][j][2 * h], acc[i][j][2 * h + 1]);
+                        double2 o = make_double2(acc[i][j][2 * h], acc[i][j][2 * h + 1]);
+                        if constexpr (SUB) {
+                            const double2 cur = *reinterpret_cast<const double2*>(dst);
+                            o = make_double2(cur.x - o.x, cur.y - o.y);
+                        }
+                        *reinterpret_cast<double2*>(dst) = o;
                     } else if (c < N) {
-                        dst[0] = acc[i][j][2 * h];
+                        dst[0] = SUB ? dst[0] - acc[i][j][2 * h] : acc[i][j][2 * h];
                     }
                 }
             }
@@ -633,6 +639,25 @@ static fb_status launch_f64(int64_t m, int64_t n, int64_t k, const void* A, int6
     }
     kern<<<grid, CF::THREADS, CF::SMEM, s>>>((const double*)A, (const double*)B, (double*)C, m, n, k, lda, ldb, ldc);
     FB_LAUNCH_CHECK("gemm_f64_dmma_kernel");
+    return FB_OK;
+}
+
+// C -= A B in FP64 (LU trailing update; C may alias neither A nor B).
+fb_status gemm_f64_sub_device(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                              int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
+    using CF = f64::CfgSmall;
+    auto kern = f64::gemm_f64_dmma_kernel<CF, true>;
+    static int attr_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_mask & (1 << (dev & 31)))) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+        attr_mask |= 1 << (dev & 31);
+    }
+    if (m <= 0 || n <= 0 || k <= 0) return FB_OK;
+    dim3 grid((unsigned)((n + CF::BN - 1) / CF::BN), (unsigned)((m + CF::BM - 1) / CF::BM));
+    kern<<<grid, CF::THREADS, CF::SMEM, s>>>(A, B, C, m, n, k, lda, ldb, ldc);
+    FB_LAUNCH_CHECK("gemm_f64_dmma_kernel<sub>");
     return FB_OK;
 }
 

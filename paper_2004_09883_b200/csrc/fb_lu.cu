@@ -1,0 +1,288 @@
+// fb_lu.cu -- the paper's own matrix workload: LU decomposition with partial pivoting
+// ("LU decomposition processing of 2048*2048 orthogonal matrix data", PAPER.md P:153,
+// replaced there by cuSOLVER getrf).  P A = L U in place, FP64,
+// row-major, LAPACK getrf semantics (first max |a| pivot, whole-row swaps, ipiv 0-based).
+//
+// Blocked right-looking factorisation with 8-column panels:
+//   1. lu_panel_kernel   one CTA: the panel's rows live in registers (4 rows x 8 columns per
+//                        thread); per column: pivot search (warp shuffles + block reduction,
+//                        ties to the smaller row), row swap through shared memory, division by
+//                        the pivot and the rank-1 update of the panel's remaining columns;
+//   2. lu_swap_trsm_kernel  the panel's swaps applied, in order, to every other column, then
+//                        U12 = L11^-1 A12 (unit lower 8x8) for the columns right of the panel;
+//   4. A22 -= A21 U12    the DMMA GEMM with a subtracting epilogue (fb_gemm.cu).
+#include <float.h>
+
+#include "fb_common.cuh"
+
+namespace fb {
+fb_status gemm_f64_sub_device(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
+                              int64_t ldb, double* C, int64_t ldc, cudaStream_t s);
+
+namespace lu {
+constexpr int NB = 8;       // panel width
+constexpr int NMAX = 4096;  // n <= 4096
+
+// Panel factorisation, one CTA: PT threads, each holding RPT rows (tid + i*PT) x PNB columns
+// of the panel in registers; the panel is staged through shared memory so the global loads
+// and stores are coalesced 16-byte transfers.  Per column: local scan, warp max by shuffles
+// with LAPACK's tie rule (smallest row among equal maxima, __reduce_min_sync), every warp
+// reduces the per-warp results itself, pivot/row-c copies through parity-buffered shared
+// slots -> two block barriers per column.
+template <int PT, int RPT, int PNB>
+__global__ void __launch_bounds__(PT, 1)
+    lu_panel_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int32_t* __restrict__ ipiv,
+                    int32_t* __restrict__ info) {
+    constexpr int NW = PT / 32;
+    __shared__ double red_v[2][NW];
+    __shared__ int red_r[2][NW];
+    __shared__ double prow[2][PNB], crow[2][PNB];
+    static_assert(PNB <= NB, "panel width");
+    extern __shared__ __align__(16) double P[];  // [m][PNB]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the previous update has finished
+    const int m = n - j0;
+    for (int e = tid; e < m * (PNB / 2); e += PT) {
+        const int r = e / (PNB / 2), ch = e % (PNB / 2);
+        double2 v = make_double2(0.0, 0.0);
+        if (2 * ch < jb) v = *reinterpret_cast<const double2*>(A + (int64_t)(j0 + r) * lda + j0 + 2 * ch);
+        if (2 * ch + 1 >= jb) v.y = 0.0;
+        *reinterpret_cast<double2*>(P + r * PNB + 2 * ch) = v;
+    }
+    __syncthreads();
+    double a[RPT][PNB];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int rr = tid + i * PT;
+#pragma unroll
+        for (int j = 0; j < PNB; ++j) a[i][j] = rr < m ? P[rr * PNB + j] : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < PNB; ++k) {  // unrolled: register indices are constants
+        if (k >= jb) break;
+        const int par = k & 1;
+        const int c = j0 + k;
+        double bv = -1.0;
+        int br = INT_MAX;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {  // rows ascend with i: strict > keeps the first max
+            const int r = j0 + tid + i * PT;
+            const double v = fabs(a[i][k]);
+            if (r >= c && r < n && v > bv) {
+                bv = v;
+                br = r;
+            }
+        }
+        double wv = bv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wv = fmax(wv, __shfl_xor_sync(0xffffffffu, wv, o));
+        const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == wv ? br : INT_MAX));
+        if (lane == 0) {
+            red_v[par][warp] = wv;
+            red_r[par][warp] = wr;
+        }
+        __syncthreads();
+        double pv = -1.0;
+        int p = INT_MAX;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {  // every thread: same order, same result
+            const double v = red_v[par][w];
+            const int r = red_r[par][w];
+            if (v > pv || (v == pv && r < p)) {
+                pv = v;
+                p = r;
+            }
+        }
+        if (tid == 0) ipiv[c] = p;
+        const int oc = (c - j0) % PT, ic = (c - j0) / PT;
+        const int op = (p - j0) % PT, ip = (p - j0) / PT;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            if (tid == op && i == ip)
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) prow[par][j] = a[i][j];
+            if (tid == oc && i == ic)
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) crow[par][j] = a[i][j];
+        }
+        __syncthreads();
+        if (p != c) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                if (tid == oc && i == ic)
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) a[i][j] = prow[par][j];
+                if (tid == op && i == ip)
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) a[i][j] = crow[par][j];
+            }
+        }
+        const double piv = prow[par][k];
+        if (piv == 0.0) {
+            if (tid == 0 && *info == 0) *info = c + 1;  // singular column: skipped, as LAPACK
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = j0 + tid + i * PT;
+                if (r > c && r < n) {
+                    const double l = a[i][k] / piv;
+                    a[i][k] = l;
+#pragma unroll
+                    for (int j = k + 1; j < PNB; ++j)
+                        if (j < jb) a[i][j] -= l * prow[par][j];
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int rr = tid + i * PT;
+        if (rr < m)
+#pragma unroll
+            for (int j = 0; j < PNB; ++j) P[rr * PNB + j] = a[i][j];
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    for (int e = tid; e < m * (PNB / 2); e += PT) {
+        const int r = e / (PNB / 2), ch = e % (PNB / 2);
+        const double2 v = *reinterpret_cast<const double2*>(P + r * PNB + 2 * ch);
+        double* dst = A + (int64_t)(j0 + r) * lda + j0 + 2 * ch;
+        if (2 * ch + 1 < jb)
+            *reinterpret_cast<double2*>(dst) = v;
+        else if (2 * ch < jb)
+            dst[0] = v.x;
+    }
+}
+
+// Per column outside the panel: the panel's swaps applied in order, then (for the columns
+// right of the panel) the forward substitution U12 = L11^-1 A12 with the unit-lower L11.
+constexpr int SWAP_T = 128;
+__global__ void __launch_bounds__(SWAP_T)
+    lu_swap_trsm_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb,
+                        const int32_t* __restrict__ ipiv) {
+    __shared__ double L[NB][NB];
+    __shared__ int piv[NB];
+    asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the panel kernel has finished
+    if (threadIdx.x < NB * NB) {
+        const int i = threadIdx.x / NB, k = threadIdx.x % NB;
+        L[i][k] = (i < jb && k < jb) ? A[(int64_t)(j0 + i) * lda + j0 + k] : 0.0;
+    }
+    if (threadIdx.x < NB) piv[threadIdx.x] = threadIdx.x < jb ? ipiv[j0 + threadIdx.x] : j0 + threadIdx.x;
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int col = blockIdx.x * SWAP_T + threadIdx.x;
+    if (col >= n || (col >= j0 && col < j0 + jb)) return;
+#pragma unroll 1
+    for (int k = 0; k < jb; ++k) {
+        const int p = piv[k];
+        if (p != j0 + k) {
+            const double t = A[(int64_t)(j0 + k) * lda + col];
+            A[(int64_t)(j0 + k) * lda + col] = A[(int64_t)p * lda + col];
+            A[(int64_t)p * lda + col] = t;
+        }
+    }
+    if (col < j0 + jb) return;
+    double x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = i < jb ? A[(int64_t)(j0 + i) * lda + col] : 0.0;
+#pragma unroll
+    for (int i = 1; i < NB; ++i)
+#pragma unroll
+        for (int k = 0; k < i; ++k) x[i] -= L[i][k] * x[k];
+#pragma unroll
+    for (int i = 1; i < NB; ++i)
+        if (i < jb) A[(int64_t)(j0 + i) * lda + col] = x[i];
+}
+}  // namespace lu
+
+size_t lu_ws_bytes(int64_t) { return 0; }
+
+// Launch with programmatic stream serialization (each LU kernel waits on griddepcontrol.wait
+// before touching the matrix, so its launch overlaps the previous kernel's tail).
+template <typename Kern, typename... Args>
+static fb_status lu_launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    static bool attr_set = false;
+    if (smem > 48 * 1024 && !attr_set) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_kernel<512, 4, lu::NB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * lu::NB * 8));
+        FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_kernel<1024, 4, lu::NB / 2>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (lu::NB / 2) * 8));
+        attr_set = true;
+    }
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+    FB_LAUNCH_CHECK("lu kernel");
+    return FB_OK;
+}
+
+fb_status lu_device(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
+    FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
+    const bool small = n <= 2048;
+    const int nb = small ? lu::NB : lu::NB / 2;
+    for (int64_t j0 = 0; j0 < n; j0 += nb) {
+        const int jb = (int)((n - j0) < nb ? (n - j0) : nb);
+        if (small)
+            FB_TRY(lu_launch(lu::lu_panel_kernel<512, 4, lu::NB>, dim3(1), dim3(512),
+                             (size_t)(n - j0) * lu::NB * sizeof(double), s, A, lda, (int)n, (int)j0, jb, ipiv, info));
+        else
+            FB_TRY(lu_launch(lu::lu_panel_kernel<1024, 4, lu::NB / 2>, dim3(1), dim3(1024),
+                             (size_t)(n - j0) * (lu::NB / 2) * sizeof(double), s, A, lda, (int)n, (int)j0, jb, ipiv,
+                             info));
+        FB_TRY(lu_launch(lu::lu_swap_trsm_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
+                         dim3(lu::SWAP_T), 0, s, A, lda,
+                         (int)n, (int)j0, jb, (const int32_t*)ipiv));
+        const int64_t rest = n - j0 - jb;
+        if (rest > 0) {
+            double* A21 = A + (j0 + jb) * lda + j0;
+            double* U12 = A + j0 * lda + j0 + jb;
+            double* A22 = A + (j0 + jb) * lda + j0 + jb;
+            FB_TRY(gemm_f64_sub_device(rest, rest, jb, A21, lda, U12, lda, A22, lda, s));
+        }
+    }
+    return FB_OK;
+}
+
+}  // namespace fb
+
+using namespace fb;
+
+extern "C" {
+
+size_t fb_lu_workspace_bytes(int dtype, int64_t n) { return (dtype == FB_F64 && n > 0) ? lu_ws_bytes(n) : 0; }
+
+fb_status fb_lu(int dtype, int64_t n, void* A, int64_t lda, int32_t* ipiv, int32_t* info, void* ws, size_t ws_bytes,
+                void* stream) {
+    clear_error();
+    (void)ws;
+    (void)ws_bytes;
+    if (dtype != FB_F64) {
+        set_error("fb_lu: only FB_F64 is implemented");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (n <= 0 || !A || !ipiv || !info || lda < n) {
+        set_error("fb_lu: bad arguments");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (n > lu::NMAX) {
+        set_error("fb_lu: n <= %d supported", lu::NMAX);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    if (!aligned16(A) || (lda * 8) % 16) {
+        set_error("fb_lu: A must be 16-byte aligned with lda even");
+        return FB_ERR_MISALIGNED;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    return lu_device(n, (double*)A, lda, ipiv, info, (cudaStream_t)stream);
+}
+
+}  // extern "C"

@@ -37,4 +37,6 @@ for dt in (torch.float32, torch.float64):
 torch.backends.cuda.matmul.allow_tf32 = True
 a = torch.randn(2048, 2048, device="cuda")
 out["cublas_tf32_2048_ms"] = t(lambda: a @ a)
+q = torch.randn(2048, 2048, dtype=torch.float64, device="cuda")
+out["cusolver_getrf_f64_2048_ms"] = t(lambda: torch.linalg.lu_factor(q))
 print(json.dumps(out))
