@@ -252,6 +252,19 @@ struct Stages {
 #ifndef FB_FFT_THREADS_PER_SM
 #define FB_FFT_THREADS_PER_SM 1024  // occupancy target -> register cap 65536 / this
 #endif
+// First step of a 2 x (N/2) four-step split of the column length, fused into the row pass:
+// lane pairs (c = 0, 1) hold rows q and q + N/2 of the same column positions; X[0] = x0 + x1
+// goes to row q, X[1] = (x0 - x1) W_N^q to row q + N/2.
+template <int E>
+__device__ __forceinline__ void pair_radix2(float2* v, int c, int64_t q, int log2N, const float2* __restrict__ tw) {
+    const float2 w = __ldg(tw + ((q << (kTwLog2 - log2N)) & (kTwN - 1)));
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[m].x, 1), __shfl_xor_sync(0xffffffffu, v[m].y, 1));
+        v[m] = (c == 0) ? cadd(v[m], o) : cmul(csub(o, v[m]), w);
+    }
+}
+
 template <int LOG2L, int C, int MODE>
 __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
                                   (C * LineGeom<LOG2L>::T >= FB_FFT_THREADS_PER_SM) ? 1
@@ -302,6 +315,9 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
     }
 
     Stages<LOG2L, C, 0>::run(v, sm, t, c, stw, nullptr);
+    if constexpr (C % 2 == 0) {
+        if (p.pair_log2N > 0) pair_radix2<G::E>(v, c & 1, gh, p.pair_log2N, tw);  // nlines even: both lanes valid
+    }
 
     if (!valid) return;
     if (p.tw4_log2N > 0) {
@@ -457,28 +473,29 @@ static int pick_C(int log2L, bool col_like) {
 // =====================================================================================
 enum { KIND_ROW = 1, KIND_COL = 2 };
 
-template <int LOG2L, int C, int KIND>
+template <int LOG2L, int C, int KIND, int NB = 2>
 struct TmaGeom {
     using G = LineGeom<LOG2L>;
     static constexpr int PADS = (KIND == KIND_ROW && C > 1) ? 16 / C : 0;  // S line pad (row kind)
     static constexpr int SLINE = G::L + PADS;
     static constexpr int S_ELEMS = (KIND == KIND_ROW) ? C * SLINE : C * G::L;
     static constexpr int X_ELEMS = C * G::PADL;
-    static constexpr size_t SMEM = (size_t)(2 * S_ELEMS + X_ELEMS) * sizeof(float2) + 64;
+    static constexpr size_t SMEM = (size_t)(NB * S_ELEMS + X_ELEMS) * sizeof(float2) + 64;
     static constexpr int BOX = G::L < 256 ? G::L : 256;  // COL: elements per TMA box
 };
 
-template <int LOG2L, int C, int KIND, bool OUT_GENERIC>
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB>
 __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, 1)
     fft_pass_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap tin,
                         const __grid_constant__ CUtensorMap tout, const float2* __restrict__ tw,
                         const float2* __restrict__ stw, int64_t ngroups, int64_t nh_in) {
     using G = LineGeom<LOG2L>;
-    using TG = TmaGeom<LOG2L, C, KIND>;
+    using TG = TmaGeom<LOG2L, C, KIND, NB>;
+    static_assert(NB == 1 || NB == 2, "one or two staging buffers");
     constexpr int L = G::L, T = G::T, E = G::E;
     extern __shared__ __align__(128) float2 smf[];
     float2* Sbuf = smf;
-    float2* X = smf + 2 * TG::S_ELEMS;
+    float2* X = smf + NB * TG::S_ELEMS;
     uint64_t* bars = reinterpret_cast<uint64_t*>(X + TG::X_ELEMS);
     const int tid = threadIdx.x;
     const int c = tid % C;
@@ -527,17 +544,18 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, 1)
         }
     };
 
-    if (tid == 0) {
+    const bool dbg_noload = (p.debug & 2) != 0;
+    if (tid == 0 && !dbg_noload) {
         if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
-        if ((int64_t)blockIdx.x + gridDim.x < ngroups) issue((int64_t)blockIdx.x + gridDim.x, 1);
+        if (NB == 2 && (int64_t)blockIdx.x + gridDim.x < ngroups) issue((int64_t)blockIdx.x + gridDim.x, 1);
     }
     (void)nh_in;
 
     int it = 0;
     for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
-        const int buf = it & 1;
+        const int buf = (NB == 2) ? (it & 1) : 0;
         const float2* S = Sbuf + buf * TG::S_ELEMS;
-        ptx::mbar_wait(ptx::smem_u32(&bars[buf]), (uint32_t)(it >> 1) & 1u);
+        if (!dbg_noload) ptx::mbar_wait(ptx::smem_u32(&bars[buf]), (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u);
         float2 v[E];
         if constexpr (KIND == KIND_COL) {
             const float2* sp = S + t * C + c;
@@ -559,15 +577,19 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, 1)
             if (tid == 0) ptx::bulk_wait_read0();  // previous group's TMA store has read X
         }
         __syncthreads();  // S[buf] consumed by everyone; X free
-        if (tid == 0) {
-            const int64_t nxt = grp + 2 * (int64_t)gridDim.x;
+        if (tid == 0 && !dbg_noload) {
+            const int64_t nxt = grp + NB * (int64_t)gridDim.x;
             if (nxt < ngroups) issue(nxt, buf);
         }
 
-        Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
+        if (!(p.debug & 1)) Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
+        if (p.debug & 4) continue;
 
         const int64_t g = grp * C + c;
         const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
+        if constexpr (C % 2 == 0) {
+            if (p.pair_log2N > 0) pair_radix2<E>(v, c & 1, gh, p.pair_log2N, tw);
+        }
         if (p.tw4_log2N > 0) {
             const int tw4 = p.tw4_log2N;
 #pragma unroll
@@ -657,11 +679,11 @@ static bool make_col_map(CUtensorMap* m, const void* base, int64_t glo, int64_t 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int LOG2L, int C, int KIND, bool OUT_GENERIC>
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB = 2>
 static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
-    using TG = TmaGeom<LOG2L, C, KIND>;
+    using TG = TmaGeom<LOG2L, C, KIND, NB>;
     constexpr int threads = C * LineGeom<LOG2L>::T;
-    auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC>;
+    auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC, NB>;
     static int attr_done_mask = 0;
     static int occ[32] = {0};
     int dev = 0;
@@ -722,14 +744,17 @@ static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic)
         out_generic = false;
         return true;
     }
-    if (!p.col_like && p.lin.es == 1 && p.lout.lo == 0 && p.lin.lo == 0) {
+    // row lines; the pair plan addresses line g = 2q + c at q*hi + c*lo (lo = n0/2 rows)
+    const bool lo_ok = (p.lout.lo == 0 && p.lin.lo == 0) ||
+                       (p.pair_log2N > 0 && (p.lin.lo * 8) % 16 == 0 && (p.lout.lo * 8) % 16 == 0);
+    if (!p.col_like && p.lin.es == 1 && lo_ok) {
         if (fft_knob("FB_FFT_NO_TMA_ROW", 0)) return false;
         const int seg = in_plain ? (1 << l) : (1 << p.lin.kb_shift);
         if (seg < 2) return false;
         if ((p.lin.hi * 8) % 16) return false;
         if (!in_plain && (p.lin.bs * 8) % 16) return false;
         if (p.lout.es != 1) return false;
-        C = 1;
+        C = p.pair_log2N > 0 ? 2 : 1;
         kind = KIND_ROW;
         out_generic = !out_plain;
         return true;
@@ -741,13 +766,18 @@ template <int LOG2L>
 static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const DeviceState* st, cudaStream_t s) {
     constexpr int T = LineGeom<LOG2L>::T;
     if (kind == KIND_COL) {
-        if (C == 2) return launch_tma_one<LOG2L, 2, KIND_COL, false>(p, st, s);
-        if (C == 4) return launch_tma_one<LOG2L, 4, KIND_COL, false>(p, st, s);
+        const bool nb1 = fft_knob("FB_FFT_COL_NB", 2) == 1;
+        if (C == 2) return nb1 ? launch_tma_one<LOG2L, 2, KIND_COL, false, 1>(p, st, s)
+                               : launch_tma_one<LOG2L, 2, KIND_COL, false>(p, st, s);
+        if (C == 4) return nb1 ? launch_tma_one<LOG2L, 4, KIND_COL, false, 1>(p, st, s)
+                               : launch_tma_one<LOG2L, 4, KIND_COL, false>(p, st, s);
         if constexpr (8 * T <= 1024 && LOG2L <= 11)
             if (C == 8) return launch_tma_one<LOG2L, 8, KIND_COL, false>(p, st, s);
         if constexpr (16 * T <= 1024 && LOG2L <= 10)
             if (C == 16) return launch_tma_one<LOG2L, 16, KIND_COL, false>(p, st, s);
     } else {
+        if (C == 2) return fft_knob("FB_FFT_ROW_NB", 2) == 1 ? launch_tma_one<LOG2L, 2, KIND_ROW, false, 1>(p, st, s)
+                                                              : launch_tma_one<LOG2L, 2, KIND_ROW, false>(p, st, s);
         return og ? launch_tma_one<LOG2L, 1, KIND_ROW, true>(p, st, s)
                   : launch_tma_one<LOG2L, 1, KIND_ROW, false>(p, st, s);
     }
@@ -757,10 +787,41 @@ static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const 
 
 static bool g_fft_tma_disabled() { return fft_knob("FB_FFT_NO_TMA", 0) == 1; }
 
-fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t s) {
-    if (p.nlines <= 0) return FB_OK;
+fb_status launch_fft_pass(const FftPass& p_in, const DeviceState* st, cudaStream_t s) {
+    if (p_in.nlines <= 0) return FB_OK;
+    FftPass p = p_in;
+    p.debug = fft_knob("FB_FFT_DEBUG", 0);
     int kind = 0, tc = 0;
     bool og = false;
+    if (p.pair_log2N > 0) {
+        // pair-plan row pass: lane pairs c = 0, 1 hold rows q, q + n0/2.  TMA kernel when the
+        // pass is expressible (A/B at 2048^2: 22 us vs 28 us for the plain kernel with C = 2);
+        // FB_FFT_PAIR_TMA=0 forces the plain kernel.
+        if (fft_knob("FB_FFT_PAIR_TMA", 1) && !g_fft_tma_disabled() && tma_eligible(p, kind, tc, og) && tc == 2 &&
+            !og) {
+            switch (p.log2L) {
+                case 6: return launch_tma_L<6>(p, kind, tc, og, st, s);
+                case 7: return launch_tma_L<7>(p, kind, tc, og, st, s);
+                case 8: return launch_tma_L<8>(p, kind, tc, og, st, s);
+                case 9: return launch_tma_L<9>(p, kind, tc, og, st, s);
+                case 10: return launch_tma_L<10>(p, kind, tc, og, st, s);
+                case 11: return launch_tma_L<11>(p, kind, tc, og, st, s);
+                case 12: return launch_tma_L<12>(p, kind, tc, og, st, s);
+            }
+        }
+        const int pc = pick_C(p.log2L, false);
+        switch (p.log2L) {
+            case 6: return launch_L<6>(p, pc < 2 ? 2 : pc, st, s);
+            case 7: return launch_L<7>(p, pc < 2 ? 2 : pc, st, s);
+            case 8: return launch_L<8>(p, pc < 2 ? 2 : pc, st, s);
+            case 9: return launch_L<9>(p, pc < 2 ? 2 : pc, st, s);
+            case 10: return launch_L<10>(p, 2, st, s);
+            case 11: return launch_L<11>(p, 2, st, s);
+            case 12: return launch_L<12>(p, 2, st, s);
+        }
+        set_error("internal: pair-plan row length 2^%d", p.log2L);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
     if (!g_fft_tma_disabled() && tma_eligible(p, kind, tc, og)) {
         switch (p.log2L) {
             case 6: return launch_tma_L<6>(p, kind, tc, og, st, s);
@@ -870,14 +931,61 @@ fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, 
     return launch_fft_pass(p3, st, s);
 }
 
+// "Pair" plan for 2^9 <= n0 <= 2^12 (knob FB_FFT_PAIR=0 disables): the column length splits as
+// 2 x n0/2; the radix-2 step rides in the row pass (lane shuffle + twiddle), so the column
+// pass works on n0/2-long lines with twice as wide TMA rows (A/B at 2048^2: 16-byte rows
+// cost 22 us, 32-byte rows 16.5 us).  Needs an n0 x n1 workspace (out-of-place column pass).
+static bool use_pair_plan(int64_t n0, int64_t n1) {
+    const int l0 = ilog2(n0), l1 = ilog2(n1);
+    return fft_knob("FB_FFT_PAIR", 1) != 0 && l0 >= 9 && l0 <= fft_knob("FB_FFT_PAIR_MAX_LOG2", 11) &&
+           l0 <= max_onchip_col() && l1 >= 6 && l1 <= 12;
+}
+
 size_t fft2d_ws_bytes(int64_t n0, int64_t n1) {
-    if (ilog2(n0) <= max_onchip_col()) return 0;
+    if (ilog2(n0) <= max_onchip_col() && !use_pair_plan(n0, n1)) return 0;
     return (size_t)n0 * (size_t)n1 * sizeof(float2);
 }
 
 fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
                        size_t ws_bytes, const DeviceState* st, cudaStream_t s, bool unscaled) {
     const float scale = (inverse && !unscaled) ? 1.0f / (float)((double)n0 * (double)n1) : 1.0f;
+    if (use_pair_plan(n0, n1) && aligned16(x) && aligned16(y) && aligned16(ws)) {
+        if (ws_bytes < fft2d_ws_bytes(n0, n1)) {
+            set_error("workspace too small");
+            return FB_ERR_WORKSPACE;
+        }
+        const int64_t half = n0 / 2;
+        float2* w = (float2*)ws;
+        // pass 1: row FFTs of the pair (q, q + n0/2) + radix-2 across the pair + W_n0^{q k_a}
+        FftPass p{};
+        p.in = (const float2*)x;
+        p.out = w;
+        p.log2L = ilog2(n1);
+        p.nlines = n0;
+        p.g_shift = 1;  // g = 2q + c -> row q + c n0/2
+        p.lin = plain_map(n1, half * n1, 1);
+        p.lout = plain_map(n1, half * n1, 1);
+        p.conj_in = inverse;
+        p.scale = 1.f;
+        p.col_like = 0;
+        p.pair_log2N = ilog2(n0);
+        FB_TRY(launch_fft_pass(p, st, s));
+        // pass 2: for k_a in {0, 1}: length-n0/2 column FFTs over rows n0/2 k_a + n_b,
+        // output X[k_a + 2 k_b] at row k_a + 2 k_b
+        const int lc = ilog2(n1);
+        FftPass p3{};
+        p3.in = w;
+        p3.out = (float2*)y;
+        p3.log2L = ilog2(half);
+        p3.nlines = 2 * n1;
+        p3.g_shift = lc;  // g = k_a * n1 + c
+        p3.lin = plain_map(half * n1, 1, n1);
+        p3.lout = plain_map(n1, 1, 2 * n1);
+        p3.conj_out = inverse;
+        p3.scale = scale;
+        p3.col_like = 1;
+        return launch_fft_pass(p3, st, s);
+    }
     const bool four_step = ilog2(n0) > max_onchip_col();
     float2* rowout = four_step ? (float2*)ws : (float2*)y;
     if (four_step && ws_bytes < fft2d_ws_bytes(n0, n1)) {

@@ -52,7 +52,8 @@ def test_fft_validation_without_device(L):
     # partial overlap: x = 16, y = 24 (sizes 128 bytes)
     assert L.fb_ifft2d(ctypes.c_void_p(16), ctypes.c_void_p(32), 4, 4, None, 0, None) == 1
     # workspace rules
-    assert L.fb_fft2d_workspace_bytes(2048, 2048) == 0
+    assert L.fb_fft2d_workspace_bytes(256, 256) == 0            # one column pass, in place
+    assert L.fb_fft2d_workspace_bytes(2048, 2048) == 2048 * 2048 * 8  # 2 x 1024 split plan
     assert L.fb_fft2d_workspace_bytes(8192, 64) == 8192 * 64 * 8
     assert L.fb_fft2d(p, ctypes.c_void_p(1 << 40), 8192, 64, None, 0, None) == 4
 

@@ -32,7 +32,8 @@ def test_slab_world1_equals_fft2d(env, n0, n1):
     comm.fb_fft2d_slab(x, y, n0, n1)
     ref = fb.fft2d(x)
     torch.cuda.synchronize()
-    assert torch.equal(y, ref)
+    # same definition; the single-GPU call may use a different column split (pair plan)
+    assert oracle.rel_l2(y.cpu().numpy(), ref.cpu().numpy()) < 5e-7
     z = torch.empty_like(x)
     comm.fb_ifft2d_slab(y, z, n0, n1)
     torch.cuda.synchronize()

@@ -198,3 +198,20 @@ def test_nr_fourn_shim(fb, n0, n1):
     z = data[1:].view(np.complex64).reshape(n0, n1)
     assert oracle.rel_l2(z, (n0 * n1) * x.astype(np.complex128)) < 5e-7
     assert data[0] == 0.0  # the unused NR slot is untouched
+
+
+@pytest.mark.parametrize("n0,n1", [(512, 64), (512, 256), (1024, 4096), (2048, 2048), (4096, 512)])
+def test_pair_plan_matches_plain_plan(fb, n0, n1, monkeypatch):
+    """The 2 x n0/2 column split (radix-2 fused into the row pass) against the one-column-pass
+    plan (FB_FFT_PAIR=0): both are the same DFT, forward and inverse."""
+    monkeypatch.setenv("FB_FFT_PAIR_MAX_LOG2", "12")
+    x = torch.from_numpy(synth.complex_field(n0, n1)).cuda()
+    y_pair = fb.fft2d(x)
+    z_pair = fb.ifft2d(y_pair)
+    monkeypatch.setenv("FB_FFT_PAIR", "0")
+    y_plain = fb.fft2d(x)
+    z_plain = fb.ifft2d(y_plain)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(y_pair.cpu().numpy(), y_plain.cpu().numpy()) < 5e-7
+    assert oracle.rel_l2(z_pair.cpu().numpy(), x.cpu().numpy()) < 5e-7
+    assert oracle.rel_l2(z_plain.cpu().numpy(), x.cpu().numpy()) < 5e-7
