@@ -35,22 +35,35 @@ def needs_build() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False, out: str | None = None, extra: list[str] | None = None) -> str:
-    """Compile libfb.so (or `out` with extra nvcc flags, for experiments)."""
+    """Compile libfb.so (or `out` with extra nvcc flags, for experiments).  Each .cu compiles
+    in its own nvcc process (in parallel), then one link step."""
+    from concurrent.futures import ThreadPoolExecutor
     so = out or SO
     if out is None and not force and not needs_build():
         return SO
     nd = nccl_dir()
-    cmd = [NVCC, "-shared", "-Xcompiler", "-fPIC", "-std=c++17", "-O3", "-lineinfo",
-           "-gencode", "arch=compute_100a,code=sm_100a",
-           "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
-           "-Xptxas", "-v" if verbose else "-O3",
-           *(extra or []), "-o", so + ".tmp", *sources(),
-           "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
-           "-Xlinker", "-rpath=" + os.path.join(nd, "lib"),
-           "-cudart", "static"]
+    flags = ["-Xcompiler", "-fPIC", "-std=c++17", "-O3", "-lineinfo",
+             "-gencode", "arch=compute_100a,code=sm_100a",
+             "-I", os.path.join(ROOT, "include"), "-I", os.path.join(nd, "include"),
+             "-Xptxas", "-v" if verbose else "-O3", *(extra or [])]
+    tag = os.path.basename(so).replace(".", "_")
+    objdir = os.path.join(HERE, "build", tag)
+    os.makedirs(objdir, exist_ok=True)
+    objs = [os.path.join(objdir, os.path.basename(src)[:-3] + ".o") for src in sources()]
+    cmds = [[NVCC, "-c", *flags, "-o", o, src] for src, o in zip(sources(), objs)]
     if verbose:
-        print(" ".join(cmd), file=sys.stderr)
-    subprocess.check_call(cmd)
+        for c in cmds:
+            print(" ".join(c), file=sys.stderr)
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        procs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    for c, pr in zip(cmds, procs):
+        sys.stderr.write(pr.stderr)
+        if pr.returncode != 0:
+            raise subprocess.CalledProcessError(pr.returncode, c)
+    link = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", so + ".tmp", *objs,
+            "-L", os.path.join(nd, "lib"), "-l:libnccl.so.2",
+            "-Xlinker", "-rpath=" + os.path.join(nd, "lib"), "-cudart", "static"]
+    subprocess.check_call(link)
     os.replace(so + ".tmp", so)
     return so
 

@@ -1,0 +1,6 @@
+// FFT pass kernels for line lengths 2^{12} (see fb_fft_kern.cuh)
+#include "fb_fft_kern.cuh"
+
+namespace fb {
+FB_FFT_INSTANTIATE_L(12)
+}  // namespace fb

@@ -1,0 +1,849 @@
+// fb_fft_kern.cuh -- kernels of the Fourier-transform function block on sm_100a.
+//
+// A 2D DFT is computed as passes of batched 1D FFTs along "lines" (rows, then columns),
+// which is the separable identity of the DFT definition (oracle/oracle.c evaluates the
+// same definition naively).  One pass = one kernel launch:
+//
+//   * a CTA owns C whole lines, so every pass may run in place (the CTA reads all of its
+//     lines before it writes any of them, and no other CTA touches them);
+//   * lines are addressed through a LineMap (row lines, column lines, the per-peer blocks of
+//     the slab all-to-all, the strided sub-lines of a four-step split), so packing and
+//     unpacking are fused into the loads/stores of a pass instead of extra HBM passes;
+//   * thread (c, t) of a line of length L = 16*T holds 16 elements k = t + m*T in registers.
+//     The first Stockham stage runs straight from global memory, the last one stores
+//     straight to global memory, and only the 1-2 middle exchanges go through shared memory
+//     (padded k + k/16 layout, interleaved by line: conflict-free for every stage);
+//   * radix-16 (and one radix-2/4/8 tail stage) butterflies are fully unrolled in registers;
+//     twiddles come from one 16384-entry FP32 table built in FP64 (fb_api.cu);
+//   * the inverse uses conj(FFT(conj x)) / N, so one kernel serves both signs and the exact
+//     power-of-two scale 1/(n0 n1) is fused into the last pass.
+//
+// Stockham autosort (mixed radix): stage with radix R after Ns = product of earlier radices,
+// butterfly j reads x[j + r L/R] (r < R), multiplies by W_{Ns R}^{(j mod Ns) r}, applies the
+// radix-R DFT, writes y[(j / Ns) Ns R + (j mod Ns) + r Ns].  Output is in natural order.
+#pragma once
+#include <cuda.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include "fb_common.cuh"
+#include "fb_ptx.cuh"
+
+namespace fb {
+
+// Complex arithmetic on interleaved (re, im) pairs with the sm_100 packed-FP32 instructions
+// (FADD2 / FMUL2 / FFMA2; operand broadcast, lane swap and per-lane negation are free
+// operand modifiers), so a complex add is one instruction and a complex multiply two.
+// Every lane is IEEE RN, identical to the scalar forms.
+__device__ __forceinline__ float2 bc2(float v) { return make_float2(v, v); }
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __ffma2_rn(b, bc2(-1.f), a); }
+// a * w  = a.x (w.x, w.y) + a.y (-w.y, w.x)
+__device__ __forceinline__ float2 cmul(float2 a, float2 w) {
+    const float2 t = __fmul2_rn(bc2(a.x), w);
+    return __ffma2_rn(make_float2(-w.y, w.x), bc2(a.y), t);
+}
+// a + (-i) b = (a.x + b.y, a.y - b.x)   and   a - (-i) b = (a.x - b.y, a.y + b.x)
+__device__ __forceinline__ float2 cadd_mi(float2 a, float2 b) {
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(1.f, -1.f), a);
+}
+__device__ __forceinline__ float2 csub_mi(float2 a, float2 b) {
+    return __ffma2_rn(make_float2(b.y, b.x), make_float2(-1.f, 1.f), a);
+}
+// x * (c - i s) = c x + s (x.y, -x.x)
+__device__ __forceinline__ float2 cmul_cs(float2 x, float c, float s) {
+    const float2 t = __fmul2_rn(x, bc2(c));
+    return __ffma2_rn(make_float2(x.y, x.x), make_float2(s, -s), t);
+}
+
+// Radix-2 combine of the DIT recursion with the compile-time twiddle W_R^K = exp(-2 pi i K/R):
+// v[K] = e + W o, v[K + R/2] = e - W o.  K = 0 and K = R/4 (-i) need no multiply.
+template <int K, int R>
+__device__ __forceinline__ void butterfly(float2* v, float2 e, float2 o) {
+    constexpr float kS = 0.707106781186547524400844362104849039f;   // cos(pi/4)
+    constexpr float kC1 = 0.923879532511286756128183189396788933f;  // cos(pi/8)
+    constexpr float kS1 = 0.382683432365089771728459984030398866f;  // sin(pi/8)
+    if constexpr (K == 0) {
+        v[K] = cadd(e, o);
+        v[K + R / 2] = csub(e, o);
+    } else if constexpr (4 * K == R) {
+        v[K] = cadd_mi(e, o);
+        v[K + R / 2] = csub_mi(e, o);
+    } else {
+        // theta = 2 pi K / R in (0, pi), K != R/4; cos/sin as RN FP32 constants
+        constexpr float c = (8 * K == R) ? kS : (8 * K == 3 * R) ? -kS
+                          : (16 * K == R) ? kC1 : (16 * K == 3 * R) ? kS1
+                          : (16 * K == 5 * R) ? -kS1 : -kC1;
+        constexpr float s = (8 * K == R || 8 * K == 3 * R) ? kS
+                          : (16 * K == R || 16 * K == 7 * R) ? kS1 : kC1;
+        static_assert(8 * K == R || 8 * K == 3 * R || 16 * K == R || 16 * K == 3 * R || 16 * K == 5 * R ||
+                          16 * K == 7 * R,
+                      "radix > 16 not supported");
+        const float2 t = cmul_cs(o, c, s);
+        v[K] = cadd(e, t);
+        v[K + R / 2] = csub(e, t);
+    }
+}
+
+template <int R, int K>
+struct Combine {
+    __device__ __forceinline__ static void run(float2* v, const float2* e, const float2* o) {
+        if constexpr (K < R / 2) {
+            butterfly<K, R>(v, e[K], o[K]);
+            Combine<R, K + 1>::run(v, e, o);
+        }
+    }
+};
+
+// In-register DFT: v[k] <- sum_r v[r] exp(-2 pi i r k / R), natural order in and out.
+template <int R>
+__device__ __forceinline__ void dft(float2* v) {
+    if constexpr (R == 1) {
+        return;
+    } else if constexpr (R == 2) {
+        const float2 a = v[0], b = v[1];
+        v[0] = cadd(a, b);
+        v[1] = csub(a, b);
+    } else {
+        float2 e[R / 2], o[R / 2];
+#pragma unroll
+        for (int i = 0; i < R / 2; ++i) {
+            e[i] = v[2 * i];
+            o[i] = v[2 * i + 1];
+        }
+        dft<R / 2>(e);
+        dft<R / 2>(o);
+        Combine<R, 0>::run(v, e, o);
+    }
+}
+
+template <int LOG2L>
+struct LineGeom {
+    static constexpr int L = 1 << LOG2L;
+    static constexpr int E = L < 16 ? L : 16;       // elements per thread
+    static constexpr int T = L / E;                 // threads per line
+    static constexpr int S16 = LOG2L >= 4 ? LOG2L / 4 : 0;
+    static constexpr int REM = LOG2L >= 4 ? LOG2L % 4 : LOG2L;
+    // stage radices: S16 stages of 16, then one stage of 2^REM (if REM > 0)
+    static constexpr int NSTAGES = S16 + (REM > 0 ? 1 : 0);
+    static constexpr int PADL = L + (L >> 4);       // padded line length in smem
+};
+
+// Padded shared-memory position of element k of a line (one pad slot per 16 elements).
+__host__ __device__ constexpr int padk(int k) { return k + (k >> 4); }
+
+// ---- per-stage twiddle tables (built once per device by fb_init, see stage_tw_index()):
+// for line length 2^l and stage s >= 1 (radix R, Ns = 16^s), entries [r][jm] = W_{Ns R}^{jm r},
+// r < R, jm < Ns: a warp's lanes (consecutive jm) read consecutive entries for each r, and a
+// thread reaches its R twiddles at immediate offsets r*Ns from one base pointer.
+__host__ __device__ constexpr int stage_radix(int l, int s) {
+    return (s < (l >= 4 ? l / 4 : 0)) ? 16 : (1 << (l >= 4 ? l % 4 : l));
+}
+__host__ __device__ constexpr int stage_count(int l) {
+    return (l >= 4 ? l / 4 : 0) + (((l >= 4 ? l % 4 : l) > 0) ? 1 : 0);
+}
+__host__ __device__ constexpr int64_t stage_tw_size(int l, int s) {
+    return (s == 0) ? 0 : (int64_t(1) << (4 * s)) * stage_radix(l, s);
+}
+__host__ __device__ constexpr int64_t stage_tw_offset(int l, int s) {
+    int64_t off = 0;
+    for (int ll = 0; ll < l; ++ll)
+        for (int ss = 1; ss < stage_count(ll); ++ss) off += stage_tw_size(ll, ss);
+    for (int ss = 1; ss < s; ++ss) off += stage_tw_size(l, ss);
+    return off;
+}
+
+// Twiddles of stage S for this thread's butterflies j = t + q T: tw[q][r-1] = W_{Ns R}^{(j mod Ns) r}.
+template <int LOG2L, int S>
+struct StageTw {
+    static constexpr int R = stage_radix(LOG2L, S);
+    static constexpr int Q = LineGeom<LOG2L>::E / R;
+    static constexpr int NT = (S == 0) ? 1 : Q * (R - 1);
+    __device__ __forceinline__ static void load(float2* tw, int t, const float2* __restrict__ stw) {
+        if constexpr (S > 0) {
+            constexpr int Ns = 1 << (4 * S);
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                const int jm = (t + q * LineGeom<LOG2L>::T) & (Ns - 1);
+                const float2* twp = stw + stage_tw_offset(LOG2L, S) + jm;
+#pragma unroll
+                for (int r = 1; r < R; ++r) tw[q * (R - 1) + r - 1] = __ldg(twp + r * Ns);
+            }
+        }
+    }
+};
+
+// Stage `S` (0-based): radix R, Ns = 16^S.  v[m] holds element t + m T of the stage input
+// on entry (stage 0: loaded by the caller) and of the stage output on exit.  `tw` holds this
+// stage's twiddles, prefetched by the previous stage just before its barrier (the element
+// registers are dead there, so the loads overlap the barrier and the exchange reads).
+template <int LOG2L, int C, int S>
+struct Stages {
+    using G = LineGeom<LOG2L>;
+    __device__ __forceinline__ static void run(float2* v, float2* sm, int t, int c,
+                                               const float2* __restrict__ stw, const float2* tw) {
+        if constexpr (S < G::NSTAGES) {
+            constexpr int R = stage_radix(LOG2L, S);
+            constexpr int Ns = 1 << (4 * S);
+            constexpr int Q = G::E / R;  // butterflies per thread in this stage
+            constexpr int T = G::T;
+            constexpr bool first = (S == 0);
+            constexpr bool last = (S == G::NSTAGES - 1);
+            if constexpr (!first) {
+                // read x[t + m T]
+                if constexpr (T % 16 == 0) {
+                    const float2* rp = sm + padk(t) * C + c;
+#pragma unroll
+                    for (int m = 0; m < G::E; ++m) v[m] = rp[m * (T + T / 16) * C];
+                } else {
+#pragma unroll
+                    for (int m = 0; m < G::E; ++m) v[m] = sm[padk(t + m * T) * C + c];
+                }
+            }
+            // butterflies j = t + q T (q < Q), inputs v[q + r Q] = x[j + r L/R]
+#pragma unroll
+            for (int q = 0; q < Q; ++q) {
+                float2 b[R];
+#pragma unroll
+                for (int r = 0; r < R; ++r) b[r] = v[q + r * Q];
+                if constexpr (!first) {
+#pragma unroll
+                    for (int r = 1; r < R; ++r) b[r] = cmul(b[r], tw[q * (R - 1) + r - 1]);
+                }
+                dft<R>(b);
+#pragma unroll
+                for (int r = 0; r < R; ++r) v[q + r * Q] = b[r];
+            }
+            if constexpr (!last) {
+                static_assert(Q == 1 && R == 16, "only the last stage may be a tail stage");
+                if constexpr (!first) __syncthreads();  // everyone has read the buffer
+                // write y[(t / Ns) Ns R + (t mod Ns) + r Ns]
+                if constexpr (Ns == 1) {
+                    float2* wp = sm + (17 * t) * C + c;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) wp[r * C] = v[r];
+                } else {
+                    const int kb = (t / Ns) * Ns * R + (t & (Ns - 1));
+                    float2* wp = sm + padk(kb) * C + c;
+#pragma unroll
+                    for (int r = 0; r < R; ++r) wp[r * (Ns + Ns / 16) * C] = v[r];
+                }
+                float2 twn[StageTw<LOG2L, S + 1>::NT];
+                StageTw<LOG2L, S + 1>::load(twn, t, stw);
+                __syncthreads();
+                Stages<LOG2L, C, S + 1>::run(v, sm, t, c, stw, twn);
+            }
+        }
+    }
+};
+
+#ifndef FB_FFT_THREADS_PER_SM
+#define FB_FFT_THREADS_PER_SM 1024  // occupancy target -> register cap 65536 / this
+#endif
+// First step of a 2 x (N/2) four-step split of the column length, fused into the row pass:
+// lane pairs (c = 0, 1) hold rows q and q + N/2 of the same column positions; X[0] = x0 + x1
+// goes to row q, X[1] = (x0 - x1) W_N^q to row q + N/2.
+__device__ __forceinline__ float2 pair_twiddle(int64_t q, int log2N, const float2* __restrict__ tw) {
+    return __ldg(tw + ((q << (kTwLog2 - log2N)) & (kTwN - 1)));
+}
+template <int E>
+__device__ __forceinline__ void pair_radix2(float2* v, int c, float2 w) {
+#pragma unroll
+    for (int m = 0; m < E; ++m) {
+        const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[m].x, 1), __shfl_xor_sync(0xffffffffu, v[m].y, 1));
+        v[m] = (c == 0) ? cadd(v[m], o) : cmul(csub(o, v[m]), w);
+    }
+}
+
+template <int LOG2L, int C, int MODE>
+__global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
+                                  (C * LineGeom<LOG2L>::T >= FB_FFT_THREADS_PER_SM) ? 1
+                                  : (FB_FFT_THREADS_PER_SM / (C * LineGeom<LOG2L>::T) > 32)
+                                      ? 32
+                                      : FB_FFT_THREADS_PER_SM / (C * LineGeom<LOG2L>::T))
+    fft_pass_kernel(const FftPass p, const float2* __restrict__ tw, const float2* __restrict__ stw) {
+    using G = LineGeom<LOG2L>;
+    extern __shared__ float2 sm[];
+    const int tid = threadIdx.x;
+    const int c = tid % C;
+    const int t = tid / C;
+    const int64_t g = (int64_t)blockIdx.x * C + c;
+    const bool valid = g < p.nlines;
+    const int64_t gh = (p.g_shift >= 62) ? 0 : (g >> p.g_shift);
+    const int64_t gl = (p.g_shift >= 62) ? g : (g & ((int64_t(1) << p.g_shift) - 1));
+
+    const float2* src = p.in + gh * p.lin.hi + gl * p.lin.lo;
+    float2* dst = p.out + gh * p.lout.hi + gl * p.lout.lo;
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();  // PDL: the previous pass's output is complete and visible
+
+    float2 v[G::E];
+    if constexpr (MODE == 1) {
+        const float2* sp = src + t;
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) v[m] = valid ? sp[m * G::T] : make_float2(0.f, 0.f);
+    } else if constexpr (MODE == 2) {
+        const char* sp = reinterpret_cast<const char*>(src + (int64_t)t * p.lin.es);
+        const int64_t step = (int64_t)G::T * p.lin.es * (int64_t)sizeof(float2);
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            v[m] = valid ? *reinterpret_cast<const float2*>(sp) : make_float2(0.f, 0.f);
+            sp += step;
+        }
+    } else {
+        const int in_kmask = (1 << p.lin.kb_shift) - 1;
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            const int k = t + m * G::T;
+            const int64_t off = (int64_t)(k & in_kmask) * p.lin.es + (int64_t)(k >> p.lin.kb_shift) * p.lin.bs;
+            v[m] = valid ? src[off] : make_float2(0.f, 0.f);
+        }
+    }
+    if (p.conj_in) {
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) v[m].y = -v[m].y;
+    }
+
+    float2 wpair = make_float2(1.f, 0.f);
+    if constexpr (C % 2 == 0) {
+        if (p.pair_log2N > 0) wpair = pair_twiddle(gh, p.pair_log2N, tw);
+    }
+    Stages<LOG2L, C, 0>::run(v, sm, t, c, stw, nullptr);
+    if constexpr (C % 2 == 0) {
+        if (p.pair_log2N > 0) pair_radix2<G::E>(v, c & 1, wpair);  // nlines even: both lanes valid
+    }
+
+    if (!valid) return;
+    if (p.tw4_log2N > 0) {
+        // four-step twiddle W_N^{gh k}, N = 2^tw4 (the master table has resolution 2^14)
+        const int tw4 = p.tw4_log2N;
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            const int k = t + m * G::T;
+            const int64_t e = (gh * (int64_t)k) & ((int64_t(1) << tw4) - 1);
+            v[m] = cmul(v[m], __ldg(tw + (e << (kTwLog2 - tw4))));
+        }
+    }
+    if (p.conj_out) {
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) v[m].y = -v[m].y;
+    }
+    if (p.scale != 1.0f) {
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            v[m].x *= p.scale;
+            v[m].y *= p.scale;
+        }
+    }
+    if constexpr (MODE == 1) {
+        float2* dp = dst + t;
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) dp[m * G::T] = v[m];
+    } else if constexpr (MODE == 2) {
+        char* dp = reinterpret_cast<char*>(dst + (int64_t)t * p.lout.es);
+        const int64_t step = (int64_t)G::T * p.lout.es * (int64_t)sizeof(float2);
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            *reinterpret_cast<float2*>(dp) = v[m];
+            dp += step;
+        }
+    } else {
+        const int out_kmask = (1 << p.lout.kb_shift) - 1;
+#pragma unroll
+        for (int m = 0; m < G::E; ++m) {
+            const int k = t + m * G::T;
+            const int64_t off = (int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs;
+            dst[off] = v[m];
+        }
+    }
+}
+
+// Tuning knobs read once from the environment (for A/B measurements; defaults are the tuned
+// configuration).
+static int fft_knob(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+static bool fft_pdl_enabled() { return fft_knob("FB_FFT_NO_PDL", 0) == 0; }
+
+// Launch with programmatic stream serialization: the kernel may start while the previous
+// kernel on the stream drains; every FFT kernel calls pdl_wait() before touching global memory.
+template <typename Kern, typename... Args>
+static fb_status launch_pdl(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = fft_pdl_enabled() ? 1 : 0;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, args...));
+    FB_LAUNCH_CHECK("fft pass");
+    return FB_OK;
+}
+
+template <int LOG2L, int C, int MODE>
+static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    using G = LineGeom<LOG2L>;
+    constexpr int threads = C * G::T;
+    static_assert(threads <= 1024, "CTA too large");
+    const size_t smem = (G::NSTAGES > 1) ? (size_t)C * G::PADL * sizeof(float2) : 0;
+    static int attr_done_mask = 0;  // per-device bit (devices 0..31)
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (smem > 48 * 1024 && !(attr_done_mask & (1 << (dev & 31)))) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(fft_pass_kernel<LOG2L, C, MODE>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr_done_mask |= 1 << (dev & 31);
+    }
+    const int64_t blocks = (p.nlines + C - 1) / C;
+    if (blocks > 0x7fffffff) {
+        set_error("FFT pass grid too large (%lld CTAs)", (long long)blocks);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    FB_TRY(launch_pdl(fft_pass_kernel<LOG2L, C, MODE>, dim3((unsigned)blocks), dim3(threads), smem, s, p,
+                      (const float2*)st->twiddles, (const float2*)st->stage_tw));
+    return FB_OK;
+}
+
+template <int LOG2L, int C>
+static fb_status launch_LC(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    const bool plain = p.lin.kb_shift >= LOG2L && p.lout.kb_shift >= LOG2L;
+    if (plain && p.lin.es == 1 && p.lout.es == 1) return launch_one<LOG2L, C, 1>(p, st, s);
+    if (plain) return launch_one<LOG2L, C, 2>(p, st, s);
+    return launch_one<LOG2L, C, 0>(p, st, s);
+}
+
+template <int LOG2L>
+static fb_status launch_L(const FftPass& p, int C, const DeviceState* st, cudaStream_t s) {
+    constexpr int T = LineGeom<LOG2L>::T;
+    switch (C) {
+        case 8:
+            if constexpr (8 * T <= 1024) return launch_LC<LOG2L, 8>(p, st, s);
+            break;
+        case 4:
+            if constexpr (4 * T <= 1024) return launch_LC<LOG2L, 4>(p, st, s);
+            break;
+        case 2:
+            if constexpr (2 * T <= 1024) return launch_LC<LOG2L, 2>(p, st, s);
+            break;
+        case 1:
+            return launch_LC<LOG2L, 1>(p, st, s);
+    }
+    set_error("internal: no FFT instantiation for L=2^%d C=%d", LOG2L, C);
+    return FB_ERR_UNSUPPORTED_SIZE;
+}
+
+// Lines per CTA.  Column-like passes (adjacent lines adjacent in memory) want C*8 >= 32 B
+// row segments -> C = 4 (or 8 for short lines); row passes want small CTAs (many per SM so
+// the load / compute / store phases of different CTAs overlap), at least one full warp.
+static int pick_C(int log2L, bool col_like) {
+    const int T = (1 << log2L) < 16 ? 1 : (1 << log2L) / 16;
+    int C;
+    if (col_like)
+        C = (T <= 64) ? 8 : (T <= 256 ? 4 : 1024 / T);
+    else
+        C = (T >= 32) ? 1 : 32 / T;
+    if (C > 8) C = 8;
+    if (C < 1) C = 1;
+    return C;
+}
+
+// =====================================================================================
+// Persistent, TMA-pipelined pass (the fast path).  Each CTA loops over groups of C lines;
+// while group i is transformed, the async proxy is already filling the other staging buffer
+// with group i+1 (two staging buffers, one mbarrier each), so global-load latency is hidden
+// and no LSU instruction touches the strided input:
+//   KIND_ROW: lines (or per-peer line segments) are contiguous -> 1D bulk copies
+//             (cp.async.bulk) into S[c][k]; outputs leave by coalesced direct stores.
+//   KIND_COL: lines are adjacent columns -> one 3D TMA tensor box per 256 elements into
+//             S[k][c] (32 B or 16 B row segments gathered by the TMA engine); outputs are
+//             written densely to the exchange buffer and leave by TMA tensor stores.
+// Stage 1 reads S, later stages exchange through the padded buffer X exactly as in
+// fft_pass_kernel (same arithmetic, same results bit for bit).
+// =====================================================================================
+enum { KIND_ROW = 1, KIND_COL = 2 };
+
+template <int LOG2L, int C, int KIND, int NB = 2>
+struct TmaGeom {
+    using G = LineGeom<LOG2L>;
+    static constexpr int PADS = (KIND == KIND_ROW && C > 1) ? 16 / C : 0;  // S line pad (row kind)
+    static constexpr int SLINE = G::L + PADS;
+    static constexpr int S_ELEMS = (KIND == KIND_ROW) ? C * SLINE : C * G::L;
+    static constexpr int X_ELEMS = C * G::PADL;
+    static constexpr size_t SMEM = (size_t)(NB * S_ELEMS + X_ELEMS) * sizeof(float2) + 64;
+    static constexpr int BOX = G::L < 256 ? G::L : 256;  // COL: elements per TMA box
+};
+
+// Occupancy policy of the persistent pass: CTAs of <= 256 threads are compiled for 3 per SM
+// (register cap 85; the 16-element line code needs ~80 without spills) and get one staging
+// buffer when that lets 3 fit in shared memory (A/B at 2048^2: 39 us vs 42 us with 2 CTAs/SM
+// and two buffers); larger CTAs keep 1 per SM minimum and two buffers.
+#ifndef FB_FFT_TMA_SMALL_MINB
+#define FB_FFT_TMA_SMALL_MINB 3
+#endif
+template <int THREADS>
+constexpr int tma_minb() { return THREADS <= 256 ? FB_FFT_TMA_SMALL_MINB : 1; }
+template <int LOG2L, int C, int KIND>
+constexpr int tma_nb() {
+    return (C * LineGeom<LOG2L>::T <= 256 && 3 * (TmaGeom<LOG2L, C, KIND, 1>::SMEM + 1024) <= 228 * 1024) ? 1 : 2;
+}
+
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB>
+__global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<LOG2L>::T>())
+    fft_pass_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap tin,
+                        const __grid_constant__ CUtensorMap tout, const float2* __restrict__ tw,
+                        const float2* __restrict__ stw, int64_t ngroups, int64_t nh_in) {
+    using G = LineGeom<LOG2L>;
+    using TG = TmaGeom<LOG2L, C, KIND, NB>;
+    static_assert(NB == 1 || NB == 2, "one or two staging buffers");
+    constexpr int L = G::L, T = G::T, E = G::E;
+    extern __shared__ __align__(128) float2 smf[];
+    float2* Sbuf = smf;
+    float2* X = smf + NB * TG::S_ELEMS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(X + TG::X_ELEMS);
+    const int tid = threadIdx.x;
+    const int c = tid % C;
+    const int t = tid / C;
+    const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+    const int64_t gmask = (gshift >= 62) ? -1 : ((int64_t(1) << gshift) - 1);
+
+    if (tid == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bars[0]), 1);
+        ptx::mbar_init(ptx::smem_u32(&bars[1]), 1);
+        ptx::fence_mbar_init();
+        if constexpr (KIND == KIND_COL) {
+            ptx::tma_prefetch_desc(&tin);
+            ptx::tma_prefetch_desc(&tout);
+        }
+    }
+    __syncthreads();
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();  // PDL: everything above overlapped the previous grid's tail
+
+    // thread 0: start the asynchronous fill of staging buffer `buf` with group `grp`
+    auto issue = [&](int64_t grp, int buf) {
+        float2* S = Sbuf + buf * TG::S_ELEMS;
+        const uint32_t bar = ptx::smem_u32(&bars[buf]);
+        const int64_t g0 = grp * C;
+        if constexpr (KIND == KIND_COL) {
+            ptx::mbar_arrive_expect_tx(bar, (uint32_t)(C * L * sizeof(float2)));
+            const int64_t gh = (gshift >= 62) ? 0 : (g0 >> gshift);
+            const int gl = (int)(g0 & gmask);
+#pragma unroll 1
+            for (int kb = 0; kb < L; kb += TG::BOX)
+                ptx::tma_load_3d(ptx::smem_u32(S + kb * C), &tin, bar, gl, kb, (int)gh);
+        } else {
+            const int64_t nv = (p.nlines - g0) < C ? (p.nlines - g0) : C;
+            const int seg = (p.lin.kb_shift >= LOG2L) ? L : (1 << p.lin.kb_shift);
+            ptx::mbar_arrive_expect_tx(bar, (uint32_t)(nv * L * sizeof(float2)));
+            for (int cl = 0; cl < nv; ++cl) {
+                const int64_t g = g0 + cl;
+                const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
+                const float2* src = p.in + gh * p.lin.hi + (g & gmask) * p.lin.lo;
+#pragma unroll 1
+                for (int k0 = 0; k0 < L; k0 += seg)
+                    ptx::bulk_load(ptx::smem_u32(S + cl * TG::SLINE + k0), src + (int64_t)(k0 / seg) * p.lin.bs,
+                                   (uint32_t)(seg * sizeof(float2)), bar);
+            }
+        }
+    };
+
+    const bool dbg_noload = (p.debug & 2) != 0;
+    if (tid == 0 && !dbg_noload) {
+        if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+        if (NB == 2 && (int64_t)blockIdx.x + gridDim.x < ngroups) issue((int64_t)blockIdx.x + gridDim.x, 1);
+    }
+    (void)nh_in;
+
+    int it = 0;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+        float2 wpair = make_float2(1.f, 0.f);  // pair-plan twiddle, loaded before the data wait
+        if constexpr (C % 2 == 0) {
+            if (p.pair_log2N > 0) {
+                const int64_t gq = (grp * C + c) >> ((gshift >= 62) ? 62 : gshift);
+                wpair = pair_twiddle(gq, p.pair_log2N, tw);
+            }
+        }
+        const int buf = (NB == 2) ? (it & 1) : 0;
+        const float2* S = Sbuf + buf * TG::S_ELEMS;
+        if (!dbg_noload) ptx::mbar_wait(ptx::smem_u32(&bars[buf]), (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u);
+        float2 v[E];
+        if constexpr (KIND == KIND_COL) {
+            const float2* sp = S + t * C + c;
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = sp[m * T * C];
+        } else {
+            const float2* sp = S + c * TG::SLINE + t;
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = sp[m * T];
+        }
+        if (p.conj_in) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
+        }
+        // order this thread's generic-proxy reads of S[buf] before the async-proxy (TMA)
+        // refill of S[buf] that thread 0 issues after the barrier
+        ptx::fence_proxy_async_smem();
+        if constexpr (KIND == KIND_COL) {
+            if (tid == 0) ptx::bulk_wait_read0();  // previous group's TMA store has read X
+        }
+        __syncthreads();  // S[buf] consumed by everyone; X free
+        if (tid == 0 && !dbg_noload) {
+            const int64_t nxt = grp + NB * (int64_t)gridDim.x;
+            if (nxt < ngroups) issue(nxt, buf);
+        }
+
+        if (!(p.debug & 1)) Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
+        if (p.debug & 4) continue;
+
+        const int64_t g = grp * C + c;
+        const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
+        if constexpr (C % 2 == 0) {
+            if (p.pair_log2N > 0) pair_radix2<E>(v, c & 1, wpair);
+        }
+        if (p.tw4_log2N > 0) {
+            const int tw4 = p.tw4_log2N;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k = t + m * T;
+                const int64_t e = (gh * (int64_t)k) & ((int64_t(1) << tw4) - 1);
+                v[m] = cmul(v[m], __ldg(tw + (e << (kTwLog2 - tw4))));
+            }
+        }
+        if (p.conj_out) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
+        }
+        if (p.scale != 1.0f) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = __fmul2_rn(v[m], bc2(p.scale));
+        }
+        if constexpr (KIND == KIND_COL) {
+            __syncthreads();  // last stage finished reading X
+            float2* xp = X + t * C + c;
+#pragma unroll
+            for (int m = 0; m < E; ++m) xp[m * T * C] = v[m];
+            ptx::fence_proxy_async_smem();
+            __syncthreads();
+            if (tid == 0) {
+                const int64_t g0 = grp * C;
+                const int64_t gh0 = (gshift >= 62) ? 0 : (g0 >> gshift);
+                const int gl0 = (int)(g0 & gmask);
+#pragma unroll 1
+                for (int kb = 0; kb < L; kb += TG::BOX)
+                    ptx::tma_store_3d(&tout, ptx::smem_u32(X + kb * C), gl0, kb, (int)gh0);
+                ptx::bulk_commit();
+            }
+        } else {
+            if (g < p.nlines) {
+                float2* dst = p.out + gh * p.lout.hi + (g & gmask) * p.lout.lo;
+                if constexpr (!OUT_GENERIC) {
+                    float2* dp = dst + t;
+#pragma unroll
+                    for (int m = 0; m < E; ++m) dp[m * T] = v[m];
+                } else {
+                    const int out_kmask = (1 << p.lout.kb_shift) - 1;
+#pragma unroll
+                    for (int m = 0; m < E; ++m) {
+                        const int k = t + m * T;
+                        dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] =
+                            v[m];
+                    }
+                }
+            }
+        }
+    }
+    if constexpr (KIND == KIND_COL) {
+        if (tid == 0) ptx::bulk_wait0();
+    }
+}
+
+// ------------------------------------------------------------ host side of the TMA path
+typedef CUresult (*EncodeTiledFnFFT)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                     const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                     CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static EncodeTiledFnFFT fft_encoder() {
+    static EncodeTiledFnFFT fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFnFFT)f;
+    }
+    return fn;
+}
+
+// 3D view {line-lo (contiguous lines), element k (stride es), line-hi (stride hi)} of 8-byte
+// complex elements; box {C, min(L,256), 1}.
+static bool make_col_map(CUtensorMap* m, const void* base, int64_t glo, int64_t L, int64_t nh, int64_t es,
+                         int64_t hi, int C) {
+    EncodeTiledFnFFT enc = fft_encoder();
+    if (!enc) return false;
+    if (nh <= 1) hi = es * L;  // unused dimension; any legal stride
+    cuuint64_t dims[3] = {(cuuint64_t)glo, (cuuint64_t)L, (cuuint64_t)(nh < 1 ? 1 : nh)};
+    cuuint64_t strides[2] = {(cuuint64_t)(es * 8), (cuuint64_t)(hi * 8)};
+    cuuint32_t box[3] = {(cuuint32_t)C, (cuuint32_t)(L < 256 ? L : 256), 1u};
+    cuuint32_t estr[3] = {1u, 1u, 1u};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<void*>(base), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB = 2>
+static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    using TG = TmaGeom<LOG2L, C, KIND, NB>;
+    constexpr int threads = C * LineGeom<LOG2L>::T;
+    auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC, NB>;
+    static int attr_done_mask = 0;
+    static int occ[32] = {0};
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_done_mask & (1 << (dev & 31)))) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG::SMEM));
+        int nb = 0;
+        FB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, TG::SMEM));
+        occ[dev & 31] = nb < 1 ? 1 : nb;
+        attr_done_mask |= 1 << (dev & 31);
+    }
+    const int64_t ngroups = (p.nlines + C - 1) / C;
+    int64_t grid = (int64_t)st->sm_count * occ[dev & 31];
+    if (grid > ngroups) grid = ngroups;
+    CUtensorMap tin, tout;
+    memset(&tin, 0, sizeof(tin));
+    memset(&tout, 0, sizeof(tout));
+    int64_t nh = 1;
+    if (KIND == KIND_COL) {
+        const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+        const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
+        nh = (p.nlines + glo - 1) / glo;
+        if (!make_col_map(&tin, p.in, glo, int64_t(1) << LOG2L, nh, p.lin.es, p.lin.hi, C) ||
+            !make_col_map(&tout, p.out, glo, int64_t(1) << LOG2L, nh, p.lout.es, p.lout.hi, C)) {
+            set_error("cuTensorMapEncodeTiled failed for an FFT column pass");
+            return FB_ERR_CUDA;
+        }
+    }
+    FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), TG::SMEM, s, p, tin, tout,
+                      (const float2*)st->twiddles, (const float2*)st->stage_tw, ngroups, nh));
+    return FB_OK;
+}
+
+
+// Picks the TMA path when the pass is expressible; returns false to fall back.
+static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic) {
+    const int l = p.log2L;
+    if (l < 6 || l > 12) return false;  // >= 64 elements, staging fits for <= 4096
+    const bool al_in = ((uintptr_t)p.in & 15) == 0, al_out = ((uintptr_t)p.out & 15) == 0;
+    if (!al_in || !al_out) return false;
+    const bool in_plain = p.lin.kb_shift >= l, out_plain = p.lout.kb_shift >= l;
+    const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+    if (p.col_like && p.lin.lo == 1 && p.lout.lo == 1 && in_plain && out_plain) {
+        if (fft_knob("FB_FFT_NO_TMA_COL", 0)) return false;
+        // widest row segment (up to 128 B = 16 columns) whose double-buffered staging plus
+        // exchange buffer stays near 100 KiB (two CTAs per SM)
+        C = (l <= 8) ? 16 : (l == 9 ? 8 : (l == 10 ? 4 : 2));
+        const int kc = fft_knob("FB_FFT_COL_C", 0);
+        if (kc == 2 || kc == 4 || kc == 8 || kc == 16) C = kc;
+        if (C * (1 << l) / 16 > 1024 || (size_t)C * (1 << l) * 8 * 3 > 200 * 1024) return false;
+        const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
+        if (glo % C) return false;
+        if ((p.lin.es * 8) % 16 || (p.lout.es * 8) % 16) return false;
+        const int64_t nh = (p.nlines + glo - 1) / glo;
+        if (nh > 1 && ((p.lin.hi * 8) % 16 || (p.lout.hi * 8) % 16)) return false;
+        if (glo > (int64_t(1) << 31) || nh > (int64_t(1) << 31)) return false;
+        kind = KIND_COL;
+        out_generic = false;
+        return true;
+    }
+    // row lines; the pair plan addresses line g = 2q + c at q*hi + c*lo (lo = n0/2 rows)
+    const bool lo_ok = (p.lout.lo == 0 && p.lin.lo == 0) ||
+                       (p.pair_log2N > 0 && (p.lin.lo * 8) % 16 == 0 && (p.lout.lo * 8) % 16 == 0);
+    if (!p.col_like && p.lin.es == 1 && lo_ok) {
+        if (fft_knob("FB_FFT_NO_TMA_ROW", 0)) return false;
+        const int seg = in_plain ? (1 << l) : (1 << p.lin.kb_shift);
+        if (seg < 2) return false;
+        if ((p.lin.hi * 8) % 16) return false;
+        if (!in_plain && (p.lin.bs * 8) % 16) return false;
+        if (p.lout.es != 1) return false;
+        C = p.pair_log2N > 0 ? 2 : 1;
+        kind = KIND_ROW;
+        out_generic = !out_plain;
+        return true;
+    }
+    return false;
+}
+
+// Staging-buffer count: one buffer (3 CTAs/SM) when the tma_nb policy allows it and every
+// CTA then still has >= 2 groups to stream (A/B: 2048^2 38 us vs 42, 16384^2 2.97 ms vs
+// 3.05); with fewer groups per CTA (<= 1024^2) two buffers and 2 CTAs/SM avoid a serial
+// second group on a third of the CTAs (17.4 us vs 19.0 at 1024^2).  Knob (1 or 2) forces.
+template <int LOG2L, int C, int KIND>
+static fb_status launch_tma_nb(const FftPass& p, const DeviceState* st, cudaStream_t s, const char* knob) {
+    constexpr int D = tma_nb<LOG2L, C, KIND>();
+    int nb = D;
+    if constexpr (D == 1) {
+        constexpr int occ1 = (int)((228 * 1024) / (TmaGeom<LOG2L, C, KIND, 1>::SMEM + 1024));
+        const int64_t ngroups = (p.nlines + C - 1) / C;
+        if (ngroups < 2 * (int64_t)st->sm_count * (occ1 < 3 ? occ1 : 3)) nb = 2;
+    }
+    nb = fft_knob(knob, nb);
+    if (nb == 3 - D) return launch_tma_one<LOG2L, C, KIND, false, 3 - D>(p, st, s);
+    return launch_tma_one<LOG2L, C, KIND, false, D>(p, st, s);
+}
+
+template <int LOG2L>
+static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const DeviceState* st, cudaStream_t s) {
+    constexpr int T = LineGeom<LOG2L>::T;
+    if (kind == KIND_COL) {
+        if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+        if (C == 4) return launch_tma_nb<LOG2L, 4, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+        if constexpr (8 * T <= 1024 && LOG2L <= 11)
+            if (C == 8) return launch_tma_nb<LOG2L, 8, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+        if constexpr (16 * T <= 1024 && LOG2L <= 10)
+            if (C == 16) return launch_tma_nb<LOG2L, 16, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+    } else {
+        if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_ROW>(p, st, s, "FB_FFT_ROW_NB");
+        if (!og) return launch_tma_nb<LOG2L, 1, KIND_ROW>(p, st, s, "FB_FFT_ROW_NB");
+        return launch_tma_one<LOG2L, 1, KIND_ROW, true>(p, st, s);
+    }
+    set_error("internal: no TMA FFT instantiation");
+    return FB_ERR_UNSUPPORTED_SIZE;
+}
+
+static bool g_fft_tma_disabled() { return fft_knob("FB_FFT_NO_TMA", 0) == 1; }
+
+// All launches of one line length (explicitly instantiated per length in fb_fft_k*.cu so the
+// kernel variants compile in parallel translation units).
+template <int LOG2L>
+fb_status launch_pass_L(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    int kind = 0, tc = 0;
+    bool og = false;
+    constexpr bool has_tma = LOG2L >= 6 && LOG2L <= 12;
+    if (p.pair_log2N > 0) {
+        // pair-plan row pass: lane pairs c = 0, 1 hold rows q, q + n0/2.  TMA kernel when the
+        // pass is expressible (A/B at 2048^2: 22 us vs 28 us for the plain kernel with C = 2);
+        // FB_FFT_PAIR_TMA=0 forces the plain kernel.
+        if constexpr (has_tma) {
+            if (fft_knob("FB_FFT_PAIR_TMA", 1) && !g_fft_tma_disabled() && tma_eligible(p, kind, tc, og) && tc == 2 &&
+                !og)
+                return launch_tma_L<LOG2L>(p, kind, tc, og, st, s);
+        }
+        const int pc = pick_C(LOG2L, false);
+        if constexpr (LOG2L >= 6 && LOG2L <= 12) return launch_L<LOG2L>(p, pc < 2 ? 2 : pc, st, s);
+        set_error("internal: pair-plan row length 2^%d", LOG2L);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    if constexpr (has_tma) {
+        if (!g_fft_tma_disabled() && tma_eligible(p, kind, tc, og)) return launch_tma_L<LOG2L>(p, kind, tc, og, st, s);
+    }
+    return launch_L<LOG2L>(p, pick_C(LOG2L, p.col_like != 0), st, s);
+}
+
+#define FB_FFT_EXTERN_L(L) extern template fb_status launch_pass_L<L>(const FftPass&, const DeviceState*, cudaStream_t);
+#define FB_FFT_INSTANTIATE_L(L) template fb_status launch_pass_L<L>(const FftPass&, const DeviceState*, cudaStream_t);
+
+}  // namespace fb

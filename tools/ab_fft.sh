@@ -1,10 +1,6 @@
 cd $GRAFT_REPO_ROOT
 rm -f gpurun_out/ab.jsonl
-timeout 900 python -m pytest tests/test_fft_gpu.py -m gpu -q -x -k "pair or full_oracle or determin" 2>&1 | tail -3 > gpurun_out/ab_tests.log
-for n in "2048 2048" "1024 1024" "4096 4096" "512 512" "16384 16384"; do
+timeout 900 python -m pytest tests/test_fft_gpu.py tests/test_comm_gpu.py -m gpu -q -x 2>&1 | tail -3 > gpurun_out/ab_tests.log
+for n in "2048 2048" "1024 1024" "4096 4096" "256 256" "512 512" "16384 16384" "8192 8192"; do
 timeout 60 python tools/fft_pass_bench.py $n 30 >> gpurun_out/ab.jsonl 2>&1
-FB_FFT_ROW_NB=1 timeout 60 python tools/fft_pass_bench.py $n 30 >> gpurun_out/ab.jsonl 2>&1
-FB_FFT_COL_NB=1 timeout 60 python tools/fft_pass_bench.py $n 30 >> gpurun_out/ab.jsonl 2>&1
-FB_FFT_COL_NB=1 FB_FFT_ROW_NB=1 timeout 60 python tools/fft_pass_bench.py $n 30 >> gpurun_out/ab.jsonl 2>&1
 done
-FB_FFT_COL_NB=1 FB_FFT_ROW_NB=1 timeout 120 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file gpurun_out/pair.csv python tools/fft_pass_bench.py 2048 2048 3 > /dev/null 2>&1
