@@ -173,16 +173,36 @@ int fb_comm_size(const fb_comm* comm);
  * Rank r owns rows [r n0/P, (r+1) n0/P) of the natural n0 x n1 array, stored as an
  * (n0/P) x n1 row-major slab.  The forward transform returns the COLUMN slab: rank r
  * receives all n0 rows of columns [r n1/P, (r+1) n1/P) of Y, stored row-major as an
- * n0 x (n1/P) array.  One ncclAlltoAll (the global transpose) per call; the packing into
- * per-peer blocks is fused into the row pass.  fb_ifft2d_slab is the exact inverse:
- * column slab in, natural row slab out (scaled by 1/(n0 n1)).
- * Requires n0 % P == 0 and n1 % P == 0.  x and out must not overlap.
- * ws: fb_fft2d_slab_workspace_bytes(P, n0, n1) device bytes (send + receive buffers). */
+ * n0 x (n1/P) array.  fb_ifft2d_slab is the exact inverse: column slab in, natural row
+ * slab out (scaled by 1/(n0 n1)).  Requires n0 % P == 0 and n1 % P == 0.  x and out must
+ * not overlap.  ws: fb_fft2d_slab_workspace_bytes(P, n0, n1) device bytes.
+ *
+ * The global transpose runs one of two ways (same kernels, same results bit for bit):
+ *   fused (default when every rank is NVLink/NVSwitch load-store reachable -- NCCL LSA team =
+ *     world -- and NCCL symmetric memory is available): the row pass stores each column block
+ *     straight into its owner's symmetric receive window (forward), or loads it from there
+ *     (inverse), over NVLink; two NCCL device-API LSA barriers per call order the windows.
+ *     The window (n0 n1 / P elements per rank) is owned by the communicator, allocated
+ *     collectively on the first call that needs it (every rank must make the same calls).
+ *   NCCL: row pass packs per-peer blocks into ws, one ncclAlltoAll, column pass.
+ * fb_comm_fused reports the mode (1 fused, 0 NCCL; env FB_SLAB_FUSED=0 forces NCCL) and
+ * fb_comm_fused_detail why fused is off. */
 size_t fb_fft2d_slab_workspace_bytes(int nranks, int64_t n0, int64_t n1);
 fb_status fb_fft2d_slab(fb_comm* comm, const void* x_rows, void* y_cols, int64_t n0, int64_t n1,
                         void* ws, size_t ws_bytes, void* stream);
 fb_status fb_ifft2d_slab(fb_comm* comm, const void* y_cols, void* x_rows, int64_t n0, int64_t n1,
                          void* ws, size_t ws_bytes, void* stream);
+int fb_comm_fused(fb_comm* comm);
+const char* fb_comm_fused_detail(const fb_comm* comm);
+
+/* Single-GPU model of the fused slab path for P virtual ranks (test hook, no communicator):
+ * runs, rank after rank on `stream`, exactly the kernels and peer addressing the P ranks run,
+ * with rank d's receive window = win + d * (n0 n1 / P) elements (win: n0 n1 complex64).
+ * Forward: x = the full n0 x n1 array (rank r's slab = rows [r n0/P, (r+1) n0/P)); y = the P
+ * column slabs one after another ([d][n0][n1/P]).  Inverse (inverse = 1): y in, x out.
+ * ws: fb_fft2d_slab_workspace_bytes(P, n0, n1) bytes (four-step scratch). */
+fb_status fb_fft2d_slab_model(int nranks, int inverse, void* x, void* y, int64_t n0, int64_t n1, void* win,
+                              void* ws, size_t ws_bytes, void* stream);
 
 /* Row-block GEMM (north_star (4), reading R18): rank r owns A rows and C rows
  * [r m/P, (r+1) m/P) as (m/P) x k and (m/P) x n row-major blocks; B (k x n) lives on

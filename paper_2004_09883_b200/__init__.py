@@ -32,6 +32,7 @@ EXPORTS = [
     "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
     "fb_comm_size", "fb_fft2d_slab_workspace_bytes", "fb_fft2d_slab", "fb_ifft2d_slab",
+    "fb_comm_fused", "fb_comm_fused_detail", "fb_fft2d_slab_model",
     "fb_matmul_rowblock_workspace_bytes", "fb_matmul_rowblock", "fb_nr_fourn",
     "fb_lu_workspace_bytes", "fb_lu",
 ]
@@ -81,6 +82,9 @@ def lib() -> ctypes.CDLL:
         "fb_fft2d_slab_workspace_bytes": ([ci, i64, i64], sz),
         "fb_fft2d_slab": ([vp, vp, vp, i64, i64, vp, sz, vp], ci),
         "fb_ifft2d_slab": ([vp, vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_comm_fused": ([vp], ci),
+        "fb_comm_fused_detail": ([vp], ctypes.c_char_p),
+        "fb_fft2d_slab_model": ([ci, ci, vp, vp, i64, i64, vp, vp, sz, vp], ci),
         "fb_matmul_rowblock_workspace_bytes": ([ci, ci, i64, i64, i64], sz),
         "fb_matmul_rowblock": ([vp, ci, i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, vp, sz, vp], ci),
         "fb_nr_fourn": ([vp, vp, ci, ci], ci),
@@ -320,6 +324,15 @@ def _nccl_uid() -> bytes:
     return buf.raw
 
 
+def fb_fft2d_slab_model(P: int, x, y, n0: int, n1: int, inverse: bool = False, stream=None):
+    """Single-GPU model of the fused slab path for P virtual ranks (fb.h): forward x (n0 x n1)
+    -> y = the P column slabs [P][n0][n1/P]; inverse y -> x."""
+    win = torch.empty(n0 * n1, dtype=torch.complex64, device=x.device)
+    ws = _workspace_named(lib().fb_fft2d_slab_workspace_bytes(P, n0, n1), x.device, "slab_model")
+    _check("fb_fft2d_slab_model", lib().fb_fft2d_slab_model(P, int(inverse), _ptr(x), _ptr(y), n0, n1, _ptr(win),
+                                                            _ptr(ws), ws.numel(), _stream(stream)))
+
+
 class Comm:
     """An fb_comm (NCCL communicator) for this process's GPU."""
 
@@ -329,6 +342,15 @@ class Comm:
         _check("fb_comm_init", lib().fb_comm_init(ctypes.byref(handle), world, rank, raw, device))
         self.handle = handle
         self.rank, self.world, self.device = rank, world, device
+
+    @property
+    def fused(self) -> bool:
+        """True when fb_fft2d_slab moves the column blocks itself over NVLink (fused path)."""
+        return bool(lib().fb_comm_fused(self.handle))
+
+    @property
+    def fused_detail(self) -> str:
+        return lib().fb_comm_fused_detail(self.handle).decode(errors="replace")
 
     def destroy(self):
         if self.handle:

@@ -2,7 +2,19 @@
 // (north_star (4)): the slab-sharded 2D FFT whose global transpose is one NCCL all-to-all,
 // and the row-block GEMM with B broadcast.  One process per GPU; NCCL communicator from a
 // unique id the caller distributes (torch.distributed in the Python binding).
+//
+// Fused transpose: when every rank is load/store reachable over NVLink
+// (NCCL LSA team = world), each rank owns a receive window in NCCL symmetric memory and the
+// row pass moves the column blocks itself -- forward: stores element k of a local row into
+// the window of rank k / (n1/P) (push); inverse: loads it from there (pull) -- so the
+// transpose costs no staging buffer, no NCCL copy kernel and no extra HBM round trip, and
+// the NVLink traffic overlaps the FFT arithmetic tile by tile.  Ordering uses the NCCL 2.28
+// device API (ncclLsaBarrierSession, acquire/release at system scope) in two one-CTA kernels
+// per call: before the row pass (peers are done with the windows of the previous call) and
+// after it (every peer's blocks have landed).
 #include <nccl.h>
+#include <nccl_device.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "fb_common.cuh"
@@ -10,6 +22,15 @@
 struct fb_comm {
     ncclComm_t nccl = nullptr;
     int rank = 0, size = 1, device = 0;
+    // fused path
+    int fused = 0;                         // 1: LSA team == world and the device comm is up
+    char fused_why[256] = "not initialised";
+    bool devcomm_ok = false;
+    ncclDevComm devcomm{};
+    void* win_buf = nullptr;               // this rank's receive window (ncclMemAlloc)
+    size_t win_bytes = 0;
+    ncclWindow_t win = nullptr;
+    float2* peer_base[fb::kMaxPeers] = {};  // window bases of every rank, as mapped here
 };
 
 namespace fb {
@@ -76,6 +97,132 @@ static fb_status check_slab(fb_comm* c, const void* a, const void* b, int64_t n0
     return FB_OK;
 }
 
+// ---------------------------------------------------------------- fused transpose plumbing
+__global__ void lsa_barrier_kernel(ncclDevComm dc) {
+    ncclLsaBarrierSession<ncclCoopCta> bar(ncclCoopCta(), dc, ncclTeamTagLsa(), 0);
+    bar.sync(ncclCoopCta(), cuda::memory_order_acq_rel);
+}
+
+__global__ void lsa_pointers_kernel(ncclWindow_t w, int n, const int* lsa_of_rank, void** out) {
+    const int p = threadIdx.x;
+    if (p < n) out[p] = ncclGetLsaPointer(w, 0, lsa_of_rank[p]);
+}
+
+static fb_status lsa_barrier(fb_comm* c, cudaStream_t s) {
+    lsa_barrier_kernel<<<1, 32, 0, s>>>(c->devcomm);
+    FB_LAUNCH_CHECK("lsa barrier");
+    return FB_OK;
+}
+
+// Collective (called by every rank from fb_comm_init): decide whether the fused path is
+// available and create the device communicator with one LSA barrier.
+static void fused_probe(fb_comm* c) {
+    const char* e = getenv("FB_SLAB_FUSED");
+    if (e && e[0] == '0') {
+        snprintf(c->fused_why, sizeof(c->fused_why), "disabled by FB_SLAB_FUSED=0");
+        return;
+    }
+    if (c->size > kMaxPeers) {
+        snprintf(c->fused_why, sizeof(c->fused_why), "world size %d > %d", c->size, kMaxPeers);
+        return;
+    }
+    const ncclTeam_t lsa = ncclTeamLsa(c->nccl);
+    if (lsa.nRanks != c->size) {
+        snprintf(c->fused_why, sizeof(c->fused_why), "LSA team has %d of %d ranks (not one NVLink domain)",
+                 lsa.nRanks, c->size);
+        return;
+    }
+    ncclDevCommRequirements reqs;
+    memset(&reqs, 0, sizeof(reqs));
+    reqs.lsaBarrierCount = 1;
+    const ncclResult_t r = ncclDevCommCreate(c->nccl, &reqs, &c->devcomm);
+    if (r != ncclSuccess) {
+        snprintf(c->fused_why, sizeof(c->fused_why), "ncclDevCommCreate: %s (%s)", ncclGetErrorString(r),
+                 ncclGetLastError(c->nccl));
+        return;
+    }
+    c->devcomm_ok = true;
+    c->fused = 1;
+    snprintf(c->fused_why, sizeof(c->fused_why), "fused (LSA team of %d)", c->size);
+}
+
+// Collective: (re)allocate and register the receive window, then map every rank's base.
+static fb_status ensure_window(fb_comm* c, size_t bytes) {
+    if (c->win_bytes >= bytes) return FB_OK;
+    if (c->win) {
+        FB_NCCL_TRY(ncclCommWindowDeregister(c->nccl, c->win), c->nccl);
+        c->win = nullptr;
+    }
+    if (c->win_buf) {
+        FB_NCCL_TRY(ncclMemFree(c->win_buf), c->nccl);
+        c->win_buf = nullptr;
+        c->win_bytes = 0;
+    }
+    FB_NCCL_TRY(ncclMemAlloc(&c->win_buf, bytes), c->nccl);
+    FB_NCCL_TRY(ncclCommWindowRegister(c->nccl, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC), c->nccl);
+    c->win_bytes = bytes;
+    int lsa_of_rank[kMaxPeers];
+    const ncclTeam_t world = ncclTeamWorld(c->nccl);
+    for (int p = 0; p < c->size; ++p) lsa_of_rank[p] = ncclTeamRankToLsa(c->nccl, world, p);
+    void* dbuf = nullptr;
+    FB_CUDA_TRY(cudaMalloc(&dbuf, kMaxPeers * (sizeof(void*) + sizeof(int))));
+    void** dptr = (void**)dbuf;
+    int* dlsa = (int*)(dptr + kMaxPeers);
+    cudaError_t ce = cudaMemcpy(dlsa, lsa_of_rank, c->size * sizeof(int), cudaMemcpyHostToDevice);
+    if (ce == cudaSuccess) {
+        lsa_pointers_kernel<<<1, 32>>>(c->win, c->size, dlsa, dptr);
+        ce = cudaGetLastError();
+    }
+    void* host[kMaxPeers] = {};
+    if (ce == cudaSuccess) ce = cudaMemcpy(host, dptr, c->size * sizeof(void*), cudaMemcpyDeviceToHost);
+    cudaFree(dbuf);
+    if (ce != cudaSuccess) {
+        set_error("mapping the symmetric window failed: %s", cudaGetErrorString(ce));
+        return FB_ERR_CUDA;
+    }
+    for (int p = 0; p < c->size; ++p) c->peer_base[p] = (float2*)host[p];
+    return FB_OK;
+}
+
+// The fused passes, shared by the real path and the single-GPU model (fb_fft2d_slab_model).
+// win[d] = base of rank d's receive window (n0 x cols natural column strip).
+// Forward row pass of rank r: row i of the slab -> element k to win[k / cols][(r rows + i) cols + k mod cols].
+static fb_status slab_rows_push(const float2* x_rows, float2* const* win, int r, int P, int64_t n0, int64_t n1,
+                                const DeviceState* st, cudaStream_t s) {
+    const int64_t rows = n0 / P, cols = n1 / P;
+    FftPass p{};
+    p.in = x_rows;
+    p.log2L = ilog2(n1);
+    p.nlines = rows;
+    p.g_shift = 0;
+    p.lin = lmap(n1, 0, 1);
+    p.lout = lmap(cols, 0, 1, ilog2(cols), 0);
+    p.scale = 1.f;
+    for (int d = 0; d < P; ++d) p.peer[d] = win[d] + (int64_t)r * rows * cols;
+    p.out = p.peer[0];  // P == 1: one block, plain store
+    p.peer_out = P > 1;
+    return launch_fft_pass(p, st, s);
+}
+
+// Inverse row pass of rank r: element k of local row i <- win[k / cols][(r rows + i) cols + k mod cols].
+static fb_status slab_rows_pull(float2* const* win, float2* x_rows, int r, int P, int64_t n0, int64_t n1,
+                                const DeviceState* st, cudaStream_t s) {
+    const int64_t rows = n0 / P, cols = n1 / P;
+    FftPass p{};
+    p.out = x_rows;
+    p.log2L = ilog2(n1);
+    p.nlines = rows;
+    p.g_shift = 0;
+    p.lin = lmap(cols, 0, 1, ilog2(cols), 0);
+    p.lout = lmap(n1, 0, 1);
+    p.conj_out = 1;
+    p.scale = 1.0f / (float)((double)n0 * (double)n1);
+    for (int d = 0; d < P; ++d) p.peer[d] = win[d] + (int64_t)r * rows * cols;
+    p.in = p.peer[0];
+    p.peer_in = P > 1;
+    return launch_fft_pass(p, st, s);
+}
+
 }  // namespace fb
 
 using namespace fb;
@@ -116,6 +263,7 @@ fb_status fb_comm_init(fb_comm** comm, int nranks, int rank, const void* uid, in
         delete c;
         return FB_ERR_NCCL;
     }
+    fused_probe(c);
     *comm = c;
     return FB_OK;
 }
@@ -124,6 +272,18 @@ fb_status fb_comm_destroy(fb_comm* c) {
     clear_error();
     if (!c) return FB_OK;
     fb_status st = FB_OK;
+    if (c->nccl && c->win) {
+        if (ncclCommWindowDeregister(c->nccl, c->win) != ncclSuccess) st = FB_ERR_NCCL;
+        c->win = nullptr;
+    }
+    if (c->win_buf) {
+        if (ncclMemFree(c->win_buf) != ncclSuccess) st = FB_ERR_NCCL;
+        c->win_buf = nullptr;
+    }
+    if (c->nccl && c->devcomm_ok) {
+        if (ncclDevCommDestroy(c->nccl, &c->devcomm) != ncclSuccess) st = FB_ERR_NCCL;
+        c->devcomm_ok = false;
+    }
     if (c->nccl) {
         ncclResult_t r = ncclCommDestroy(c->nccl);
         if (r != ncclSuccess) {
@@ -138,6 +298,8 @@ fb_status fb_comm_destroy(fb_comm* c) {
 
 int fb_comm_rank(const fb_comm* c) { return c ? c->rank : -1; }
 int fb_comm_size(const fb_comm* c) { return c ? c->size : -1; }
+int fb_comm_fused(fb_comm* c) { return (c && c->fused) ? 1 : 0; }
+const char* fb_comm_fused_detail(const fb_comm* c) { return c ? c->fused_why : "null communicator"; }
 
 size_t fb_fft2d_slab_workspace_bytes(int nranks, int64_t n0, int64_t n1) {
     if (nranks < 1 || n0 <= 0 || n1 <= 0 || n0 % nranks) return 0;
@@ -162,6 +324,14 @@ fb_status fb_fft2d_slab(fb_comm* c, const void* x_rows, void* y_cols, int64_t n0
     const size_t slab = (size_t)rows * n1;
     float2* send = (float2*)ws;
     float2* recv = send + slab;
+    if (c->fused) {
+        FB_TRY(ensure_window(c, slab * sizeof(float2)));
+        FB_TRY(lsa_barrier(c, s));  // every peer is done with its window (previous call)
+        FB_TRY(slab_rows_push((const float2*)x_rows, c->peer_base, c->rank, P, n0, n1, st, s));
+        FB_TRY(lsa_barrier(c, s));  // every peer's blocks have landed in this rank's window
+        return fft_columns((const float2*)c->win_buf, (float2*)y_cols, n0, cols, cols, cols, false, false, 1.f,
+                           send, st, s);
+    }
 
     FftPass p{};
     p.in = (const float2*)x_rows;
@@ -191,6 +361,14 @@ fb_status fb_ifft2d_slab(fb_comm* c, const void* y_cols, void* x_rows, int64_t n
     const size_t slab = (size_t)rows * n1;
     float2* send = (float2*)ws;
     float2* recv = send + slab;
+    if (c->fused) {
+        FB_TRY(ensure_window(c, slab * sizeof(float2)));
+        FB_TRY(lsa_barrier(c, s));  // no peer still reads this rank's window (previous call)
+        FB_TRY(fft_columns((const float2*)y_cols, (float2*)c->win_buf, n0, cols, cols, cols, true, false, 1.f, send,
+                           st, s));
+        FB_TRY(lsa_barrier(c, s));  // every peer's strip is complete
+        return slab_rows_pull(c->peer_base, (float2*)x_rows, c->rank, P, n0, n1, st, s);
+    }
     // 1. column IFFTs (conj in), natural strip into `send`: rows of peer d are contiguous
     FB_TRY(fft_columns((const float2*)y_cols, send, n0, cols, cols, cols, true, false, 1.f, recv, st, s));
     // 2. global transpose back
@@ -208,6 +386,44 @@ fb_status fb_ifft2d_slab(fb_comm* c, const void* y_cols, void* x_rows, int64_t n
     p.scale = 1.0f / (float)((double)n0 * (double)n1);
     p.col_like = 0;
     return launch_fft_pass(p, st, s);
+}
+
+fb_status fb_fft2d_slab_model(int P, int inverse, void* x, void* y, int64_t n0, int64_t n1, void* win, void* ws,
+                              size_t ws_bytes, void* stream) {
+    clear_error();
+    if (P < 1 || P > kMaxPeers || n0 <= 0 || n1 <= 0 || !x || !y || !win) {
+        set_error("bad fb_fft2d_slab_model arguments");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!is_pow2(n0) || !is_pow2(n1) || n0 > kTwN || n1 > kTwN || n0 % P || n1 % P) {
+        set_error("sizes must be powers of two <= %d divisible by P", kTwN);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    const int64_t rows = n0 / P, cols = n1 / P;
+    const size_t slab = (size_t)rows * n1;
+    if (!ws || ws_bytes < 2 * slab * sizeof(float2)) {
+        set_error("slab workspace too small");
+        return FB_ERR_WORKSPACE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    cudaStream_t s = (cudaStream_t)stream;
+    float2* w[kMaxPeers];
+    for (int d = 0; d < P; ++d) w[d] = (float2*)win + (int64_t)d * slab;
+    float2* X = (float2*)x;
+    float2* Y = (float2*)y;
+    if (!inverse) {
+        for (int r = 0; r < P; ++r) FB_TRY(slab_rows_push(X + (int64_t)r * slab, w, r, P, n0, n1, st, s));
+        for (int d = 0; d < P; ++d)
+            FB_TRY(fft_columns(w[d], Y + (int64_t)d * slab, n0, cols, cols, cols, false, false, 1.f, (float2*)ws, st,
+                               s));
+    } else {
+        for (int d = 0; d < P; ++d)
+            FB_TRY(fft_columns(Y + (int64_t)d * slab, w[d], n0, cols, cols, cols, true, false, 1.f, (float2*)ws, st,
+                               s));
+        for (int r = 0; r < P; ++r) FB_TRY(slab_rows_pull(w, X + (int64_t)r * slab, r, P, n0, n1, st, s));
+    }
+    return FB_OK;
 }
 
 size_t fb_matmul_rowblock_workspace_bytes(int nranks, int dtype, int64_t m, int64_t n, int64_t k) {

@@ -87,6 +87,7 @@ struct LineMap {
     int kb_shift;
     int64_t es, bs;
 };
+constexpr int kMaxPeers = 8;  // one NVLink/NVSwitch node
 struct FftPass {
     const float2* in;
     float2* out;
@@ -102,6 +103,11 @@ struct FftPass {
     int pair_log2N; // >0: lines come in pairs (g = 2q + c, rows q and q + N/2 of an N-long column);
                     // after the row FFT, the radix-2 column butterfly across the pair and the
                     // four-step twiddle W_N^{q k_a} are applied (first step of a 2 x N/2 split)
+    // Peer mode of the fused slab transpose (fb_comm.cu): element k of a line lives in the
+    // column block d = k >> kb_shift, and block d is addressed from its own base peer[d] (a
+    // pointer into GPU d's symmetric window, NVLink load/store) instead of base + d * bs.
+    int peer_out, peer_in;
+    float2* peer[kMaxPeers];
 };
 fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t s);
 

@@ -292,11 +292,17 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
         }
     } else {
         const int in_kmask = (1 << p.lin.kb_shift) - 1;
+        const int64_t row = gh * p.lin.hi + gl * p.lin.lo;
 #pragma unroll
         for (int m = 0; m < G::E; ++m) {
             const int k = t + m * G::T;
-            const int64_t off = (int64_t)(k & in_kmask) * p.lin.es + (int64_t)(k >> p.lin.kb_shift) * p.lin.bs;
-            v[m] = valid ? src[off] : make_float2(0.f, 0.f);
+            if (p.peer_in) {  // block k >> kb_shift from its owner's window (NVLink load)
+                const float2* b = p.peer[k >> p.lin.kb_shift] + row;
+                v[m] = valid ? b[(int64_t)(k & in_kmask) * p.lin.es] : make_float2(0.f, 0.f);
+            } else {
+                const int64_t off = (int64_t)(k & in_kmask) * p.lin.es + (int64_t)(k >> p.lin.kb_shift) * p.lin.bs;
+                v[m] = valid ? src[off] : make_float2(0.f, 0.f);
+            }
         }
     }
     if (p.conj_in) {
@@ -349,11 +355,16 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
         }
     } else {
         const int out_kmask = (1 << p.lout.kb_shift) - 1;
+        const int64_t row = gh * p.lout.hi + gl * p.lout.lo;
 #pragma unroll
         for (int m = 0; m < G::E; ++m) {
             const int k = t + m * G::T;
-            const int64_t off = (int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs;
-            dst[off] = v[m];
+            if (p.peer_out) {  // block k >> kb_shift into its owner's window (NVLink store)
+                p.peer[k >> p.lout.kb_shift][row + (int64_t)(k & out_kmask) * p.lout.es] = v[m];
+            } else {
+                const int64_t off = (int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs;
+                dst[off] = v[m];
+            }
         }
     }
 }
@@ -647,11 +658,15 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
                     for (int m = 0; m < E; ++m) dp[m * T] = v[m];
                 } else {
                     const int out_kmask = (1 << p.lout.kb_shift) - 1;
+                    const int64_t row = gh * p.lout.hi + (g & gmask) * p.lout.lo;
 #pragma unroll
                     for (int m = 0; m < E; ++m) {
                         const int k = t + m * T;
-                        dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] =
-                            v[m];
+                        if (p.peer_out)  // block k >> kb_shift into its owner's window (NVLink store)
+                            p.peer[k >> p.lout.kb_shift][row + (int64_t)(k & out_kmask) * p.lout.es] = v[m];
+                        else
+                            dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] =
+                                v[m];
                     }
                 }
             }
@@ -737,6 +752,8 @@ static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStr
 static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic) {
     const int l = p.log2L;
     if (l < 6 || l > 12) return false;  // >= 64 elements, staging fits for <= 4096
+    if (p.peer_in) return false;        // peer loads take the LSU path (no bulk copies from peers)
+    if (p.peer_out && p.col_like) return false;
     const bool al_in = ((uintptr_t)p.in & 15) == 0, al_out = ((uintptr_t)p.out & 15) == 0;
     if (!al_in || !al_out) return false;
     const bool in_plain = p.lin.kb_shift >= l, out_plain = p.lout.kb_shift >= l;

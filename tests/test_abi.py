@@ -87,3 +87,13 @@ def test_comm_validation_without_device(L):
     assert L.fb_matmul_rowblock(None, 0, 8, 8, 8, p, 8, p, 8, 0, p, 8, None, 0, None) == 5
     assert L.fb_comm_destroy(None) == 0
     assert L.fb_fft2d_slab_workspace_bytes(4, 64, 32) == 2 * 16 * 32 * 8
+
+
+def test_slab_model_and_fused_query_validation(L):
+    p = ctypes.c_void_p(1 << 20)
+    assert L.fb_comm_fused(None) == 0
+    assert L.fb_comm_fused_detail(None) == b"null communicator"
+    assert L.fb_fft2d_slab_model(0, 0, p, p, 64, 64, p, p, 1 << 20, None) == 1   # P < 1
+    assert L.fb_fft2d_slab_model(9, 0, p, p, 64, 64, p, p, 1 << 20, None) == 1   # P > 8
+    assert L.fb_fft2d_slab_model(4, 0, p, p, 64, 2, p, p, 1 << 20, None) == 2    # n1 % P
+    assert L.fb_fft2d_slab_model(2, 0, p, p, 64, 64, p, p, 16, None) == 4        # workspace

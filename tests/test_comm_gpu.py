@@ -1,7 +1,9 @@
 """The multi-GPU entry points (NCCL communicator, slab FFT, row-block GEMM) on the one GPU this
-build has: world size 1 exercises fb_comm_init, the fused pack/unpack maps, ncclAlltoAll /
-ncclBroadcast and the column passes; results must equal the single-GPU calls bit for bit
-(same kernels, same order) and match the oracle."""
+build has: world size 1 exercises fb_comm_init, the NCCL device communicator, the symmetric
+window and LSA barriers of the fused transpose, the NCCL path (ncclAlltoAll / ncclBroadcast)
+and the column passes.  The P > 1 peer addressing of the fused transpose is covered by
+fb_fft2d_slab_model, which runs the P ranks' kernels one after another on this GPU with P
+local windows (no rank waits on another)."""
 import numpy as np
 import pytest
 import torch
@@ -71,3 +73,76 @@ def test_comm_validation(env):
     x = torch.zeros(6, 8, dtype=torch.complex64, device="cuda")
     with pytest.raises(fb.FbError):
         comm.fb_fft2d_slab(x, x, 6, 8)  # not a power of two
+
+
+def test_world1_is_fused(env):
+    fb, comm = env
+    assert comm.fused, comm.fused_detail
+
+
+def test_fused_equals_nccl_path_bitwise(env, monkeypatch):
+    fb, comm = env
+    monkeypatch.setenv("FB_SLAB_FUSED", "0")
+    plain = fb.Comm(0, 1, 0)
+    try:
+        assert not plain.fused and "FB_SLAB_FUSED" in plain.fused_detail
+        for n0, n1 in [(256, 256), (2048, 1024), (8192, 64)]:
+            x = torch.from_numpy(synth.complex_field(n0, n1)).cuda()
+            y1, y2 = torch.empty_like(x), torch.empty_like(x)
+            comm.fb_fft2d_slab(x, y1, n0, n1)
+            plain.fb_fft2d_slab(x, y2, n0, n1)
+            z1, z2 = torch.empty_like(x), torch.empty_like(x)
+            comm.fb_ifft2d_slab(y1, z1, n0, n1)
+            plain.fb_ifft2d_slab(y2, z2, n0, n1)
+            torch.cuda.synchronize()
+            assert torch.equal(y1, y2) and torch.equal(z1, z2), (n0, n1)
+    finally:
+        plain.destroy()
+
+
+def _assemble(y, P, n0, n1):
+    """[P][n0][n1/P] column slabs -> n0 x n1."""
+    return y.view(P, n0, n1 // P).permute(1, 0, 2).reshape(n0, n1)
+
+
+@pytest.mark.parametrize("n0,n1", [(256, 256), (2048, 2048), (64, 4096), (8192, 64), (16, 8)])
+def test_fused_model_all_P_bitwise(env, n0, n1):
+    """The fused transpose's peer addressing for P = 2, 4, 8 virtual ranks: every P computes the
+    same per-line arithmetic, so the assembled result equals P = 1 bit for bit, and P = 1
+    equals the real world-size-1 fused call."""
+    fb, comm = env
+    x = torch.from_numpy(synth.complex_field(n0, n1)).cuda()
+    ref = torch.empty_like(x)
+    comm.fb_fft2d_slab(x, ref, n0, n1)
+    for P in (1, 2, 4, 8):
+        if n0 % P or n1 % P:
+            continue
+        y = torch.empty(n0 * n1, dtype=torch.complex64, device="cuda")
+        fb.fb_fft2d_slab_model(P, x, y, n0, n1)
+        z = torch.empty_like(x)
+        fb.fb_fft2d_slab_model(P, z, y, n0, n1, inverse=True)
+        torch.cuda.synchronize()
+        assert torch.equal(_assemble(y, P, n0, n1), ref), P
+        assert oracle.rel_l2(z.cpu().numpy(), x.cpu().numpy()) < 5e-7, P
+        if P == 1:
+            zr = torch.empty_like(x)
+            comm.fb_ifft2d_slab(ref, zr, n0, n1)
+            torch.cuda.synchronize()
+            assert torch.equal(z, zr)
+        else:
+            z1 = torch.empty_like(x)
+            fb.fb_fft2d_slab_model(1, z1, y.view(P, n0, n1 // P).permute(1, 0, 2).reshape(-1).contiguous(), n0, n1,
+                                   inverse=True)
+            torch.cuda.synchronize()
+            assert torch.equal(z, z1), P
+
+
+def test_fused_model_vs_oracle(env):
+    fb, _ = env
+    n0, n1, P = 512, 256, 4
+    xh = synth.complex_field(n0, n1)
+    x = torch.from_numpy(xh).cuda()
+    y = torch.empty(n0 * n1, dtype=torch.complex64, device="cuda")
+    fb.fb_fft2d_slab_model(P, x, y, n0, n1)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(_assemble(y, P, n0, n1).cpu().numpy(), oracle.dft2d(xh)) < 5e-7
