@@ -246,12 +246,17 @@ struct Stages {
 __device__ __forceinline__ float2 pair_twiddle(int64_t q, int log2N, const float2* __restrict__ tw) {
     return __ldg(tw + ((q << (kTwLog2 - log2N)) & (kTwN - 1)));
 }
+// Branch-free: lane c computes (o + s v) * w_c with s = +1, w_0 = 1 for c = 0 and s = -1,
+// w_1 = W_N^q for c = 1 (FFMA2 with s is exact; multiplying by (1, 0) is exact for finite
+// values), so both lanes run the same three packed instructions per element.
 template <int E>
 __device__ __forceinline__ void pair_radix2(float2* v, int c, float2 w) {
+    const float2 sgn = bc2(c == 0 ? 1.f : -1.f);
+    const float2 wc = (c == 0) ? make_float2(1.f, 0.f) : w;
 #pragma unroll
     for (int m = 0; m < E; ++m) {
         const float2 o = make_float2(__shfl_xor_sync(0xffffffffu, v[m].x, 1), __shfl_xor_sync(0xffffffffu, v[m].y, 1));
-        v[m] = (c == 0) ? cadd(v[m], o) : cmul(csub(o, v[m]), w);
+        v[m] = cmul(__ffma2_rn(v[m], sgn, o), wc);
     }
 }
 
