@@ -193,6 +193,247 @@ __global__ void __launch_bounds__(SWAP_T)
     for (int i = 1; i < NB; ++i)
         if (i < jb) A[(int64_t)(j0 + i) * lda + col] = x[i];
 }
+// ---------------------------------------------------------------- look-ahead variant
+// Panel k+1 is factored while the wide update of step k runs on the other SMs (second stream).
+// The panel kernel therefore first finishes its own PNB columns' share of step k -- the
+// previous panel's swaps, the unit-lower solve of rows jp..jp+PNB-1 (U12) and the rank-PNB
+// update of rows >= j0 with L21(k) -- then factors them.  Rows [jp, n) of the PNB columns are
+// staged in shared memory ([row][PNB]); per column the pivot search and swap are as in
+// lu_panel_kernel, with the pivot / row-c copies done by the owning threads only.
+template <int PT, int RPT, int PNB>
+__global__ void __launch_bounds__(PT, 1)
+    lu_panel_la_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int has_prev,
+                       int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
+    constexpr int NW = PT / 32;
+    __shared__ double red_v[2][NW];
+    __shared__ int red_r[2][NW];
+    __shared__ double prow[2][PNB], crow[2][PNB];
+    __shared__ double L11[PNB][PNB];
+    __shared__ int pv[PNB];
+    extern __shared__ __align__(16) double P[];  // rows [r0, n) x PNB
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int jp = j0 - PNB;                 // previous panel (always full width)
+    const int r0 = has_prev ? jp : j0;
+    const int mr = n - r0;                   // staged rows
+    const int m = n - j0;                    // rows of this panel's factorisation
+    for (int e = tid; e < mr * (PNB / 2); e += PT) {
+        const int r = e / (PNB / 2), ch = e % (PNB / 2);
+        double2 v = make_double2(0.0, 0.0);
+        if (2 * ch < jb) v = *reinterpret_cast<const double2*>(A + (int64_t)(r0 + r) * lda + j0 + 2 * ch);
+        if (2 * ch + 1 >= jb) v.y = 0.0;
+        *reinterpret_cast<double2*>(P + r * PNB + 2 * ch) = v;
+    }
+    if (has_prev) {
+        if (tid < PNB * PNB) {
+            const int i = tid / PNB, k = tid % PNB;
+            L11[i][k] = A[(int64_t)(jp + i) * lda + jp + k];
+        }
+        if (tid < PNB) pv[tid] = ipiv[jp + tid];
+    }
+    __syncthreads();
+    if (has_prev) {
+        if (tid < PNB) {  // column tid: previous swaps in order, then x = L11^-1 x on rows jp..
+            const int j = tid;
+#pragma unroll 1
+            for (int t = 0; t < PNB; ++t) {
+                const int q = pv[t] - r0;
+                if (q != t) {
+                    const double tmp = P[t * PNB + j];
+                    P[t * PNB + j] = P[q * PNB + j];
+                    P[q * PNB + j] = tmp;
+                }
+            }
+            double x[PNB];
+#pragma unroll
+            for (int i = 0; i < PNB; ++i) x[i] = P[i * PNB + j];
+#pragma unroll
+            for (int i = 1; i < PNB; ++i)
+#pragma unroll
+                for (int k = 0; k < i; ++k) x[i] -= L11[i][k] * x[k];
+#pragma unroll
+            for (int i = 0; i < PNB; ++i) P[i * PNB + j] = x[i];
+            if (j < jb)
+#pragma unroll
+                for (int i = 0; i < PNB; ++i) A[(int64_t)(jp + i) * lda + j0 + j] = x[i];  // U12 rows
+        }
+        __syncthreads();
+    }
+    const double* Pm = P + (r0 == j0 ? 0 : PNB * PNB);  // this panel's rows [j0, n)
+    double a[RPT][PNB];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int rr = tid + i * PT;
+#pragma unroll
+        for (int j = 0; j < PNB; ++j) a[i][j] = rr < m ? Pm[rr * PNB + j] : 0.0;
+    }
+    if (has_prev) {  // A[r][j0 + j] -= sum_t L21[r][t] U12[t][j]  (same order as the GEMM: t ascending)
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int rr = tid + i * PT;
+            if (rr < m) {
+                const double* lr = A + (int64_t)(j0 + rr) * lda + jp;
+                double l[PNB];
+#pragma unroll
+                for (int t = 0; t < PNB; t += 2) {
+                    const double2 v = *reinterpret_cast<const double2*>(lr + t);
+                    l[t] = v.x;
+                    l[t + 1] = v.y;
+                }
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) {
+                    double acc = 0.0;
+#pragma unroll
+                    for (int t = 0; t < PNB; ++t) acc = fma(l[t], P[t * PNB + j], acc);
+                    a[i][j] -= acc;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < PNB; ++k) {
+        if (k >= jb) break;
+        const int par = k & 1;
+        const int c = j0 + k;
+        double bv = -1.0;
+        int br = INT_MAX;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = j0 + tid + i * PT;
+            const double v = fabs(a[i][k]);
+            if (r >= c && r < n && v > bv) {
+                bv = v;
+                br = r;
+            }
+        }
+        double wv = bv;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) wv = fmax(wv, __shfl_xor_sync(0xffffffffu, wv, o));
+        const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == wv ? br : INT_MAX));
+        if (lane == 0) {
+            red_v[par][warp] = wv;
+            red_r[par][warp] = wr;
+        }
+        __syncthreads();
+        double pvv = -1.0;
+        int p = INT_MAX;
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            const double v = red_v[par][w];
+            const int r = red_r[par][w];
+            if (v > pvv || (v == pvv && r < p)) {
+                pvv = v;
+                p = r;
+            }
+        }
+        if (tid == 0) ipiv[c] = p;
+        const int oc = (c - j0) % PT, ic = (c - j0) / PT;
+        const int op = (p - j0) % PT, ip = (p - j0) / PT;
+        if (tid == op) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                if (i == ip)
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) prow[par][j] = a[i][j];
+        }
+        if (tid == oc) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                if (i == ic)
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) crow[par][j] = a[i][j];
+        }
+        __syncthreads();
+        if (p != c) {
+            if (tid == oc) {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i)
+                    if (i == ic)
+#pragma unroll
+                        for (int j = 0; j < PNB; ++j) a[i][j] = prow[par][j];
+            }
+            if (tid == op) {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i)
+                    if (i == ip)
+#pragma unroll
+                        for (int j = 0; j < PNB; ++j) a[i][j] = crow[par][j];
+            }
+        }
+        const double piv = prow[par][k];
+        if (piv == 0.0) {
+            if (tid == 0 && *info == 0) *info = c + 1;
+        } else {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i) {
+                const int r = j0 + tid + i * PT;
+                if (r > c && r < n) {
+                    const double l = a[i][k] / piv;
+                    a[i][k] = l;
+#pragma unroll
+                    for (int j = k + 1; j < PNB; ++j)
+                        if (j < jb) a[i][j] -= l * prow[par][j];
+                }
+            }
+        }
+    }
+    // write back rows [j0, n) straight from registers (each row: PNB contiguous doubles)
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int rr = tid + i * PT;
+        if (rr < m) {
+            double* dst = A + (int64_t)(j0 + rr) * lda + j0;
+            if (jb == PNB) {
+#pragma unroll
+                for (int j = 0; j < PNB; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(a[i][j], a[i][j + 1]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < PNB; ++j)
+                    if (j < jb) dst[j] = a[i][j];
+            }
+        }
+    }
+}
+
+// Wide part of step k (look-ahead): the panel's swaps on every column outside
+// [j0, skip_end) (left: L columns of earlier panels; right: columns beyond the next panel),
+// then U12 = L11^-1 A12 for the right columns.
+__global__ void __launch_bounds__(SWAP_T)
+    lu_swap_trsm_wide_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int skip_end,
+                             const int32_t* __restrict__ ipiv) {
+    __shared__ double L[NB][NB];
+    __shared__ int piv[NB];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    if (threadIdx.x < NB * NB) {
+        const int i = threadIdx.x / NB, k = threadIdx.x % NB;
+        L[i][k] = (i < jb && k < jb) ? A[(int64_t)(j0 + i) * lda + j0 + k] : 0.0;
+    }
+    if (threadIdx.x < NB) piv[threadIdx.x] = threadIdx.x < jb ? ipiv[j0 + threadIdx.x] : j0 + threadIdx.x;
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int col = blockIdx.x * SWAP_T + threadIdx.x;
+    if (col >= n || (col >= j0 && col < skip_end)) return;
+#pragma unroll 1
+    for (int k = 0; k < jb; ++k) {
+        const int p = piv[k];
+        if (p != j0 + k) {
+            const double t = A[(int64_t)(j0 + k) * lda + col];
+            A[(int64_t)(j0 + k) * lda + col] = A[(int64_t)p * lda + col];
+            A[(int64_t)p * lda + col] = t;
+        }
+    }
+    if (col < skip_end) return;
+    double x[NB];
+#pragma unroll
+    for (int i = 0; i < NB; ++i) x[i] = i < jb ? A[(int64_t)(j0 + i) * lda + col] : 0.0;
+#pragma unroll
+    for (int i = 1; i < NB; ++i)
+#pragma unroll
+        for (int k = 0; k < i; ++k) x[i] -= L[i][k] * x[k];
+#pragma unroll
+    for (int i = 1; i < NB; ++i)
+        if (i < jb) A[(int64_t)(j0 + i) * lda + col] = x[i];
+}
 }  // namespace lu
 
 size_t lu_ws_bytes(int64_t) { return 0; }
@@ -224,7 +465,88 @@ static fb_status lu_launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaSt
     return FB_OK;
 }
 
+// Look-ahead schedule (two streams): the caller's stream s runs the panels, an internal stream
+// w the wide updates.
+//   s:  panel_0 | rec P | wait W(k-1) | panel_{k+1} (finishes step k on its columns) | rec P ...
+//   w:  wait P | wide_k = swaps outside [j0, j0 + jb + nb) + U12 + A22 -= A21 U12 beyond the
+//       next panel | rec W[k % 2]
+// panel_{k+1} needs panel_k (stream order) and wide_{k-1} (its columns' earlier updates), not
+// wide_k, which overlaps it; wide_k needs panel_k and wide_{k-1} (stream order).  Columns
+// touched concurrently are disjoint.  A wait binds to the record enqueued before it, so one
+// P event and two alternating W events suffice.
+struct LuStreams {
+    cudaStream_t w = nullptr;
+    cudaEvent_t ev_p = nullptr, ev_w[2] = {nullptr, nullptr}, ev_fork = nullptr;
+};
+static fb_status lu_streams(LuStreams** out) {
+    thread_local static LuStreams per_dev[32];  // per host thread: concurrent fb_lu calls stay independent
+    int dev = 0;
+    FB_CUDA_TRY(cudaGetDevice(&dev));
+    LuStreams& ls = per_dev[dev & 31];
+    if (!ls.w) {
+        FB_CUDA_TRY(cudaStreamCreateWithFlags(&ls.w, cudaStreamNonBlocking));
+        FB_CUDA_TRY(cudaEventCreateWithFlags(&ls.ev_p, cudaEventDisableTiming));
+        FB_CUDA_TRY(cudaEventCreateWithFlags(&ls.ev_w[0], cudaEventDisableTiming));
+        FB_CUDA_TRY(cudaEventCreateWithFlags(&ls.ev_w[1], cudaEventDisableTiming));
+        FB_CUDA_TRY(cudaEventCreateWithFlags(&ls.ev_fork, cudaEventDisableTiming));
+    }
+    *out = &ls;
+    return FB_OK;
+}
+
+template <int PT, int RPT, int PNB>
+static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
+    constexpr int nb = PNB;
+    auto panel = lu::lu_panel_la_kernel<PT, RPT, PNB>;
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)((lu::NMAX + PNB) * PNB * sizeof(double) > 200 * 1024
+                                                   ? 200 * 1024
+                                                   : (lu::NMAX + PNB) * PNB * sizeof(double))));
+        attr = true;
+    }
+    LuStreams* ls;
+    FB_TRY(lu_streams(&ls));
+    FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
+    FB_CUDA_TRY(cudaEventRecord(ls->ev_fork, s));
+    FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_fork, 0));  // w starts after everything before the call
+    for (int64_t j0 = 0; j0 < n; j0 += nb) {
+        const int jb = (int)((n - j0) < nb ? (n - j0) : nb);
+        const int has_prev = j0 > 0;
+        const int k = (int)(j0 / nb);
+        if (k >= 2) FB_CUDA_TRY(cudaStreamWaitEvent(s, ls->ev_w[k & 1], 0));  // wide_{k-2}
+        const int64_t r0 = has_prev ? j0 - nb : j0;
+        FB_TRY(lu_launch(panel, dim3(1), dim3(PT), (size_t)(n - r0) * PNB * sizeof(double), s, A, lda, (int)n,
+                         (int)j0, jb, has_prev, ipiv, info));
+        FB_CUDA_TRY(cudaEventRecord(ls->ev_p, s));
+        // wide part of this step: everything except this panel and the next one
+        FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_p, 0));
+        const int64_t nxt = (j0 + jb < n) ? ((n - j0 - jb) < nb ? (n - j0 - jb) : nb) : 0;
+        const int64_t skip_end = j0 + jb + nxt;
+        FB_TRY(lu_launch(lu::lu_swap_trsm_wide_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
+                         dim3(lu::SWAP_T), 0, ls->w, A, lda, (int)n, (int)j0, jb, (int)skip_end,
+                         (const int32_t*)ipiv));
+        const int64_t rest_r = n - j0 - jb, rest_c = n - skip_end;
+        if (rest_r > 0 && rest_c > 0) {
+            double* A21 = A + (j0 + jb) * lda + j0;
+            double* U12 = A + j0 * lda + skip_end;
+            double* A22 = A + (j0 + jb) * lda + skip_end;
+            FB_TRY(gemm_f64_sub_device(rest_r, rest_c, jb, A21, lda, U12, lda, A22, lda, ls->w));
+        }
+        FB_CUDA_TRY(cudaEventRecord(ls->ev_w[k & 1], ls->w));
+    }
+    const int klast = (int)((n - 1) / nb);
+    FB_CUDA_TRY(cudaStreamWaitEvent(s, ls->ev_w[klast & 1], 0));  // join: the last wide part
+    return FB_OK;
+}
+
 fb_status lu_device(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
+    const char* la = getenv("FB_LU_LOOKAHEAD");
+    if (!(la && la[0] == '0')) {
+        if (n <= 2048) return lu_device_la<512, 4, lu::NB>(n, A, lda, ipiv, info, s);
+        return lu_device_la<1024, 4, lu::NB / 2>(n, A, lda, ipiv, info, s);
+    }
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     const bool small = n <= 2048;
     const int nb = small ? lu::NB : lu::NB / 2;
