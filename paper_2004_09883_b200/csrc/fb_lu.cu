@@ -315,17 +315,20 @@ __global__ void __launch_bounds__(PT, 1)
             red_r[par][warp] = wr;
         }
         __syncthreads();
-        double pvv = -1.0;
-        int p = INT_MAX;
+        // every warp combines the NW per-warp results with shuffles (order-independent: the
+        // key is (|a| descending, row ascending)), instead of every thread scanning all NW
+        double pvv = (lane < NW) ? red_v[par][lane] : -1.0;
+        int p = (lane < NW) ? red_r[par][lane] : INT_MAX;
 #pragma unroll
-        for (int w = 0; w < NW; ++w) {
-            const double v = red_v[par][w];
-            const int r = red_r[par][w];
-            if (v > pvv || (v == pvv && r < p)) {
-                pvv = v;
-                p = r;
+        for (int o = NW / 2; o > 0; o >>= 1) {
+            const double ov = __shfl_xor_sync(0xffffffffu, pvv, o);
+            const int orr = __shfl_xor_sync(0xffffffffu, p, o);
+            if (ov > pvv || (ov == pvv && orr < p)) {
+                pvv = ov;
+                p = orr;
             }
         }
+        p = __shfl_sync(0xffffffffu, p, 0);
         if (tid == 0) ipiv[c] = p;
         const int oc = (c - j0) % PT, ic = (c - j0) / PT;
         const int op = (p - j0) % PT, ip = (p - j0) / PT;
