@@ -14,6 +14,7 @@
 #include <float.h>
 
 #include "fb_common.cuh"
+#include "fb_ptx.cuh"
 
 namespace fb {
 fb_status gemm_f64_sub_device(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
@@ -197,41 +198,80 @@ __global__ void __launch_bounds__(SWAP_T)
 // Panel k+1 is factored while the wide update of step k runs on the other SMs (second stream).
 // The panel kernel therefore first finishes its own PNB columns' share of step k -- the
 // previous panel's swaps, the unit-lower solve of rows jp..jp+PNB-1 (U12) and the rank-PNB
-// update of rows >= j0 with L21(k) -- then factors them.  Rows [jp, n) of the PNB columns are
-// staged in shared memory ([row][PNB]); per column the pivot search and swap are as in
-// lu_panel_kernel, with the pivot / row-c copies done by the owning threads only.
+// update of rows >= j0 with L21(k) -- then factors them.
+//
+// One SM does all of this, so the count of L1/LSU transactions is the cost, not bytes: every
+// global access is a coalesced 16-byte chunk (PNB/2 lanes per row) moved by cp.async into
+// row-major shared buffers whose 16-byte chunks are XOR-swizzled by row (chunk c of row r at
+// c ^ ((r / rows_per_128B) mod chunks)), so the per-thread row reads and writes are bank-
+// conflict-free: the panel rows [r0, n), L21 in batches of PT rows (double-buffered, the first
+// two in flight with the panel), and the write-back (registers -> buffer -> coalesced stores).
+// Per column: pivot search (warp shuffles, LAPACK's first-max tie rule), per-warp shuffle
+// combine, swap through shared memory by the owning threads only.
+template <int PNB>
+__device__ __forceinline__ int lu_pidx(int r, int j) {
+    constexpr int CH = PNB / 2;          // 16-byte chunks per row
+    constexpr int RPL = 8 / CH;          // rows per 128-byte line
+    const int c = (j >> 1) ^ ((r / RPL) & (CH - 1));
+    return r * PNB + 2 * c + (j & 1);
+}
+
 template <int PT, int RPT, int PNB>
 __global__ void __launch_bounds__(PT, 1)
     lu_panel_la_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int has_prev,
                        int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
     constexpr int NW = PT / 32;
+    constexpr int CH = PNB / 2;
     __shared__ double red_v[2][NW];
     __shared__ int red_r[2][NW];
     __shared__ double prow[2][PNB], crow[2][PNB];
     __shared__ double L11[PNB][PNB];
+    __shared__ double Us[PNB][PNB];  // U12 rows of this panel's columns
     __shared__ int pv[PNB];
-    extern __shared__ __align__(16) double P[];  // rows [r0, n) x PNB
+    extern __shared__ __align__(16) double smem_lu[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     asm volatile("griddepcontrol.wait;" ::: "memory");
-    const int jp = j0 - PNB;                 // previous panel (always full width)
+#ifdef FB_LU_TIMING
+    long long tt[6];
+    tt[0] = clock64();
+#endif
+    const int jp = j0 - PNB;  // previous panel (always full width)
     const int r0 = has_prev ? jp : j0;
-    const int mr = n - r0;                   // staged rows
-    const int m = n - j0;                    // rows of this panel's factorisation
-    for (int e = tid; e < mr * (PNB / 2); e += PT) {
-        const int r = e / (PNB / 2), ch = e % (PNB / 2);
-        double2 v = make_double2(0.0, 0.0);
-        if (2 * ch < jb) v = *reinterpret_cast<const double2*>(A + (int64_t)(r0 + r) * lda + j0 + 2 * ch);
-        if (2 * ch + 1 >= jb) v.y = 0.0;
-        *reinterpret_cast<double2*>(P + r * PNB + 2 * ch) = v;
+    const int mr = n - r0;  // staged rows
+    const int m = n - j0;   // rows of this panel's factorisation
+    const int off = j0 - r0;
+    double* P = smem_lu;           // [mr][PNB] swizzled
+    double* Lb = smem_lu + mr * PNB;  // [2][PT][PNB] swizzled L21 batches
+    for (int e = tid; e < mr * CH; e += PT) {
+        const int r = e / CH, c = e % CH;
+        const uint32_t bytes = (2 * c + 1 < jb) ? 16u : ((2 * c < jb) ? 8u : 0u);
+        ptx::cp_async_16(ptx::smem_u32(P + lu_pidx<PNB>(r, 2 * c)), A + (int64_t)(r0 + r) * lda + j0 + (bytes ? 2 * c : 0),
+                         bytes);
     }
+    auto stage_l = [&](int i, int b) {  // L21 rows j0 + i*PT + [0, PT), columns jp..jp+PNB-1
+        for (int e = tid; e < PT * CH; e += PT) {
+            const int rr = e / CH, c = e % CH;
+            const int row = i * PT + rr;
+            const bool ok = row < m;
+            ptx::cp_async_16(ptx::smem_u32(Lb + b * PT * PNB + lu_pidx<PNB>(rr, 2 * c)),
+                             A + (int64_t)(j0 + (ok ? row : 0)) * lda + jp + 2 * c, ok ? 16u : 0u);
+        }
+    };
     if (has_prev) {
+        stage_l(0, 0);
+        if (RPT > 1) stage_l(1, 1);
         if (tid < PNB * PNB) {
             const int i = tid / PNB, k = tid % PNB;
             L11[i][k] = A[(int64_t)(jp + i) * lda + jp + k];
         }
         if (tid < PNB) pv[tid] = ipiv[jp + tid];
     }
+    ptx::cp_async_commit();
+    ptx::cp_async_wait<0>();
     __syncthreads();
+#ifdef FB_LU_TIMING
+    tt[1] = clock64();
+#endif
     if (has_prev) {
         if (tid < PNB) {  // column tid: previous swaps in order, then x = L11^-1 x on rows jp..
             const int j = tid;
@@ -239,57 +279,76 @@ __global__ void __launch_bounds__(PT, 1)
             for (int t = 0; t < PNB; ++t) {
                 const int q = pv[t] - r0;
                 if (q != t) {
-                    const double tmp = P[t * PNB + j];
-                    P[t * PNB + j] = P[q * PNB + j];
-                    P[q * PNB + j] = tmp;
+                    const double tmp = P[lu_pidx<PNB>(t, j)];
+                    P[lu_pidx<PNB>(t, j)] = P[lu_pidx<PNB>(q, j)];
+                    P[lu_pidx<PNB>(q, j)] = tmp;
                 }
             }
             double x[PNB];
 #pragma unroll
-            for (int i = 0; i < PNB; ++i) x[i] = P[i * PNB + j];
+            for (int i = 0; i < PNB; ++i) x[i] = P[lu_pidx<PNB>(i, j)];
 #pragma unroll
             for (int i = 1; i < PNB; ++i)
 #pragma unroll
                 for (int k = 0; k < i; ++k) x[i] -= L11[i][k] * x[k];
 #pragma unroll
-            for (int i = 0; i < PNB; ++i) P[i * PNB + j] = x[i];
+            for (int i = 0; i < PNB; ++i) Us[i][j] = x[i];
             if (j < jb)
 #pragma unroll
                 for (int i = 0; i < PNB; ++i) A[(int64_t)(jp + i) * lda + j0 + j] = x[i];  // U12 rows
         }
         __syncthreads();
     }
-    const double* Pm = P + (r0 == j0 ? 0 : PNB * PNB);  // this panel's rows [j0, n)
     double a[RPT][PNB];
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         const int rr = tid + i * PT;
 #pragma unroll
-        for (int j = 0; j < PNB; ++j) a[i][j] = rr < m ? Pm[rr * PNB + j] : 0.0;
+        for (int c = 0; c < CH; ++c) {
+            double2 v = make_double2(0.0, 0.0);
+            if (rr < m) v = *reinterpret_cast<const double2*>(P + lu_pidx<PNB>(off + rr, 2 * c));
+            a[i][2 * c] = v.x;
+            a[i][2 * c + 1] = v.y;
+        }
     }
-    if (has_prev) {  // A[r][j0 + j] -= sum_t L21[r][t] U12[t][j]  (same order as the GEMM: t ascending)
+#ifdef FB_LU_TIMING
+    tt[2] = clock64();
+#endif
+    if (has_prev) {  // A[r][j0 + j] -= sum_t L21[r][t] U12[t][j]
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
-            const int rr = tid + i * PT;
-            if (rr < m) {
-                const double* lr = A + (int64_t)(j0 + rr) * lda + jp;
-                double l[PNB];
+            const int b = i & 1;
+            if (i >= 2) {  // batch i (issued once batch i-2 was consumed) has landed in buffer b
+                if (i == RPT - 1)
+                    ptx::cp_async_wait<0>();
+                else
+                    ptx::cp_async_wait<1>();
+                __syncthreads();
+            }
+            double l[PNB];
 #pragma unroll
-                for (int t = 0; t < PNB; t += 2) {
-                    const double2 v = *reinterpret_cast<const double2*>(lr + t);
-                    l[t] = v.x;
-                    l[t + 1] = v.y;
-                }
+            for (int c = 0; c < CH; ++c) {
+                const double2 v = *reinterpret_cast<const double2*>(Lb + b * PT * PNB + lu_pidx<PNB>(tid, 2 * c));
+                l[2 * c] = v.x;
+                l[2 * c + 1] = v.y;
+            }
 #pragma unroll
-                for (int j = 0; j < PNB; ++j) {
-                    double acc = 0.0;
+            for (int j = 0; j < PNB; ++j) {
+                double acc = 0.0;
 #pragma unroll
-                    for (int t = 0; t < PNB; ++t) acc = fma(l[t], P[t * PNB + j], acc);
-                    a[i][j] -= acc;
-                }
+                for (int t = 0; t < PNB; ++t) acc = fma(l[t], Us[t][j], acc);
+                a[i][j] -= acc;
+            }
+            if (i + 2 < RPT) {  // refill buffer b with batch i + 2 once every thread has read it
+                __syncthreads();
+                stage_l(i + 2, b);
+                ptx::cp_async_commit();
             }
         }
     }
+#ifdef FB_LU_TIMING
+    tt[3] = clock64();
+#endif
 #pragma unroll
     for (int k = 0; k < PNB; ++k) {
         if (k >= jb) break;
@@ -380,22 +439,35 @@ __global__ void __launch_bounds__(PT, 1)
             }
         }
     }
-    // write back rows [j0, n) straight from registers (each row: PNB contiguous doubles)
+#ifdef FB_LU_TIMING
+    tt[4] = clock64();
+#endif
+    // write back rows [j0, n): registers -> P (own rows, swizzled) -> coalesced 16-byte stores
 #pragma unroll
     for (int i = 0; i < RPT; ++i) {
         const int rr = tid + i * PT;
-        if (rr < m) {
-            double* dst = A + (int64_t)(j0 + rr) * lda + j0;
-            if (jb == PNB) {
+        if (rr < m)
 #pragma unroll
-                for (int j = 0; j < PNB; j += 2) *reinterpret_cast<double2*>(dst + j) = make_double2(a[i][j], a[i][j + 1]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < PNB; ++j)
-                    if (j < jb) dst[j] = a[i][j];
-            }
-        }
+            for (int c = 0; c < CH; ++c)
+                *reinterpret_cast<double2*>(P + lu_pidx<PNB>(off + rr, 2 * c)) = make_double2(a[i][2 * c], a[i][2 * c + 1]);
     }
+    __syncthreads();
+    for (int e = tid; e < m * CH; e += PT) {
+        const int r = e / CH, c = e % CH;
+        const double2 v = *reinterpret_cast<const double2*>(P + lu_pidx<PNB>(off + r, 2 * c));
+        double* dst = A + (int64_t)(j0 + r) * lda + j0 + 2 * c;
+        if (2 * c + 1 < jb)
+            *reinterpret_cast<double2*>(dst) = v;
+        else if (2 * c < jb)
+            dst[0] = v.x;
+    }
+#ifdef FB_LU_TIMING
+    __syncthreads();
+    tt[5] = clock64();
+    if (tid == 0 && (j0 == 80 || j0 == 1024 || j0 == 1600))
+        printf("LU_TIMING j0=%d stage=%lld prevprep=%lld update=%lld columns=%lld writeback=%lld total=%lld\n", j0,
+               tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[5] - tt[0]);
+#endif
 }
 
 // Wide part of step k (look-ahead): the panel's swaps on every column outside
@@ -503,14 +575,13 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
     auto panel = lu::lu_panel_la_kernel<PT, RPT, PNB>;
     static bool attr = false;
     if (!attr) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(panel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)((lu::NMAX + PNB) * PNB * sizeof(double) > 200 * 1024
-                                                   ? 200 * 1024
-                                                   : (lu::NMAX + PNB) * PNB * sizeof(double))));
+        FB_CUDA_TRY(cudaFuncSetAttribute(panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr = true;
     }
     LuStreams* ls;
     FB_TRY(lu_streams(&ls));
+    const char* dbg_s = getenv("FB_LU_DEBUG");  // timing decomposition only (wrong results): 1 no GEMM, 2 no swap/TRSM, 4 no panel
+    const int dbg = dbg_s ? atoi(dbg_s) : 0;
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     FB_CUDA_TRY(cudaEventRecord(ls->ev_fork, s));
     FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_fork, 0));  // w starts after everything before the call
@@ -520,18 +591,19 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
         const int k = (int)(j0 / nb);
         if (k >= 2) FB_CUDA_TRY(cudaStreamWaitEvent(s, ls->ev_w[k & 1], 0));  // wide_{k-2}
         const int64_t r0 = has_prev ? j0 - nb : j0;
-        FB_TRY(lu_launch(panel, dim3(1), dim3(PT), (size_t)(n - r0) * PNB * sizeof(double), s, A, lda, (int)n,
-                         (int)j0, jb, has_prev, ipiv, info));
+        const size_t smem = (size_t)(n - r0) * PNB * sizeof(double) + (size_t)2 * PT * PNB * sizeof(double);
+        if (!(dbg & 4))
+            FB_TRY(lu_launch(panel, dim3(1), dim3(PT), smem, s, A, lda, (int)n, (int)j0, jb, has_prev, ipiv, info));
         FB_CUDA_TRY(cudaEventRecord(ls->ev_p, s));
         // wide part of this step: everything except this panel and the next one
         FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_p, 0));
         const int64_t nxt = (j0 + jb < n) ? ((n - j0 - jb) < nb ? (n - j0 - jb) : nb) : 0;
         const int64_t skip_end = j0 + jb + nxt;
-        FB_TRY(lu_launch(lu::lu_swap_trsm_wide_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
+        if (!(dbg & 2)) FB_TRY(lu_launch(lu::lu_swap_trsm_wide_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
                          dim3(lu::SWAP_T), 0, ls->w, A, lda, (int)n, (int)j0, jb, (int)skip_end,
                          (const int32_t*)ipiv));
         const int64_t rest_r = n - j0 - jb, rest_c = n - skip_end;
-        if (rest_r > 0 && rest_c > 0) {
+        if (rest_r > 0 && rest_c > 0 && !(dbg & 1)) {
             double* A21 = A + (j0 + jb) * lda + j0;
             double* U12 = A + j0 * lda + skip_end;
             double* A22 = A + (j0 + jb) * lda + skip_end;
