@@ -9,6 +9,7 @@
  */
 #include "oracle.h"
 
+#include <float.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -327,10 +328,14 @@ int oracle_lu(int64_t n, double* A, int64_t lda, int32_t* ipiv, int threads) {
             if (!info) info = (int)(k + 1);
             continue;
         }
-        /* multipliers, then the rank-1 update of the trailing matrix */
+        /* multipliers, then the rank-1 update of the trailing matrix.  As LAPACK dgetf2 (and
+           dgetrf2): scale by the reciprocal 1/piv when |piv| >= sfmin (the smallest normal,
+           DBL_MIN), divide otherwise */
+        const int use_recip = fabs(piv) >= DBL_MIN;
+        const double rpiv = 1.0 / piv;
 #pragma omp parallel for num_threads(nt) schedule(static)
         for (int64_t i = k + 1; i < n; ++i) {
-            double l = A[i * lda + k] / piv;
+            double l = use_recip ? A[i * lda + k] * rpiv : A[i * lda + k] / piv;
             A[i * lda + k] = l;
             for (int64_t j = k + 1; j < n; ++j) A[i * lda + j] -= l * A[k * lda + j];
         }

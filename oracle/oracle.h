@@ -75,7 +75,8 @@ int oracle_matmul_cols(int64_t m, int64_t n, int64_t k, const void* A, int64_t l
  * P A = L U in place on the row-major n x n double matrix A (lda), right-looking, column by
  * column exactly as LAPACK's unblocked dgetf2: at step k the pivot is the FIRST row p >= k
  * with the largest |A[p][k]|, rows k and p are swapped (whole rows), the column below the
- * diagonal is divided by the pivot, and the trailing matrix receives the rank-1 update.
+ * diagonal is scaled by the pivot's reciprocal (divided instead when |pivot| < DBL_MIN, the
+ * sfmin rule of dgetf2), and the trailing matrix receives the rank-1 update.
  * ipiv[k] = p (0-based).  Returns 0, or k+1 for the first exactly-zero pivot (the step is
  * then skipped, as in LAPACK). */
 int oracle_lu(int64_t n, double* A, int64_t lda, int32_t* ipiv, int threads);

@@ -1,7 +1,8 @@
 // fb_lu.cu -- the paper's own matrix workload: LU decomposition with partial pivoting
 // ("LU decomposition processing of 2048*2048 orthogonal matrix data", PAPER.md P:153,
 // replaced there by cuSOLVER getrf).  P A = L U in place, FP64,
-// row-major, LAPACK getrf semantics (first max |a| pivot, whole-row swaps, ipiv 0-based).
+// row-major, LAPACK getrf semantics (first max |a| pivot, whole-row swaps, multipliers scaled
+// by the pivot's reciprocal unless |pivot| < DBL_MIN as in dgetf2, ipiv 0-based).
 //
 // Blocked right-looking factorisation with 8-column panels:
 //   1. lu_panel_kernel   one CTA: the panel's rows live in registers (4 rows x 8 columns per
@@ -122,11 +123,13 @@ __global__ void __launch_bounds__(PT, 1)
         if (piv == 0.0) {
             if (tid == 0 && *info == 0) *info = c + 1;  // singular column: skipped, as LAPACK
         } else {
+            const bool recip = fabs(piv) >= DBL_MIN;  // LAPACK dgetf2's sfmin rule
+            const double rpiv = 1.0 / piv;
 #pragma unroll
             for (int i = 0; i < RPT; ++i) {
                 const int r = j0 + tid + i * PT;
                 if (r > c && r < n) {
-                    const double l = a[i][k] / piv;
+                    const double l = recip ? a[i][k] * rpiv : a[i][k] / piv;
                     a[i][k] = l;
 #pragma unroll
                     for (int j = k + 1; j < PNB; ++j)
@@ -222,9 +225,10 @@ __global__ void __launch_bounds__(PT, 1)
                        int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
     constexpr int NW = PT / 32;
     constexpr int CH = PNB / 2;
-    __shared__ double red_v[2][NW];
+    __shared__ double red_row[2][NW][PNB];  // each warp's candidate row
+    __shared__ unsigned long long red_k[2][NW];
     __shared__ int red_r[2][NW];
-    __shared__ double prow[2][PNB], crow[2][PNB];
+    __shared__ double crow[2][PNB];
     __shared__ double L11[PNB][PNB];
     __shared__ double Us[PNB][PNB];  // U12 rows of this panel's columns
     __shared__ int pv[PNB];
@@ -355,7 +359,7 @@ __global__ void __launch_bounds__(PT, 1)
         const int par = k & 1;
         const int c = j0 + k;
         double bv = -1.0;
-        int br = INT_MAX;
+        int br = INT_MAX, bi = 0;
 #pragma unroll
         for (int i = 0; i < RPT; ++i) {
             const int r = j0 + tid + i * PT;
@@ -363,57 +367,52 @@ __global__ void __launch_bounds__(PT, 1)
             if (r >= c && r < n && v > bv) {
                 bv = v;
                 br = r;
+                bi = i;
             }
         }
-        double wv = bv;
+        // pivot = (max |a|, then smallest row): |a| >= 0 orders like its IEEE bit pattern, so
+        // the warp and cross-warp reductions are three redux.sync each (max hi word, max lo
+        // word among the max-hi lanes, min row among the max lanes); "no candidate" is key 0
+        // with row INT_MAX, which a real zero pivot candidate beats on the row.  The lane that
+        // holds its warp's candidate publishes the candidate's whole row, and the owner of row c
+        // (thread k) publishes row c, before the one barrier of the column: afterwards every
+        // thread reads the pivot row from the winning warp's slot, so no second barrier.
+        unsigned long long key = bv >= 0.0 ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+        unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? br : INT_MAX));
+        if (br == wr && wr != INT_MAX) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) wv = fmax(wv, __shfl_xor_sync(0xffffffffu, wv, o));
-        const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)(bv == wv ? br : INT_MAX));
+            for (int i = 0; i < RPT; ++i)
+                if (i == bi)
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) red_row[par][warp][j] = a[i][j];
+        }
         if (lane == 0) {
-            red_v[par][warp] = wv;
+            red_k[par][warp] = ((unsigned long long)mhi << 32) | mlo;
             red_r[par][warp] = wr;
         }
-        __syncthreads();
-        // every warp combines the NW per-warp results with shuffles (order-independent: the
-        // key is (|a| descending, row ascending)), instead of every thread scanning all NW
-        double pvv = (lane < NW) ? red_v[par][lane] : -1.0;
-        int p = (lane < NW) ? red_r[par][lane] : INT_MAX;
+        if (tid == k)
 #pragma unroll
-        for (int o = NW / 2; o > 0; o >>= 1) {
-            const double ov = __shfl_xor_sync(0xffffffffu, pvv, o);
-            const int orr = __shfl_xor_sync(0xffffffffu, p, o);
-            if (ov > pvv || (ov == pvv && orr < p)) {
-                pvv = ov;
-                p = orr;
-            }
-        }
-        p = __shfl_sync(0xffffffffu, p, 0);
+            for (int j = 0; j < PNB; ++j) crow[par][j] = a[0][j];  // row c = j0 + k is thread k's row 0
+        __syncthreads();
+        key = (lane < NW) ? red_k[par][lane] : 0ull;
+        const int rw = (lane < NW) ? red_r[par][lane] : INT_MAX;
+        khi = (unsigned)(key >> 32);
+        klo = (unsigned)key;
+        mhi = __reduce_max_sync(0xffffffffu, khi);
+        mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        const int p = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? rw : INT_MAX));
         if (tid == 0) ipiv[c] = p;
-        const int oc = (c - j0) % PT, ic = (c - j0) / PT;
         const int op = (p - j0) % PT, ip = (p - j0) / PT;
-        if (tid == op) {
+        double pr[PNB];
 #pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                if (i == ip)
-#pragma unroll
-                    for (int j = 0; j < PNB; ++j) prow[par][j] = a[i][j];
-        }
-        if (tid == oc) {
-#pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                if (i == ic)
-#pragma unroll
-                    for (int j = 0; j < PNB; ++j) crow[par][j] = a[i][j];
-        }
-        __syncthreads();
+        for (int j = 0; j < PNB; ++j) pr[j] = red_row[par][op >> 5][j];
         if (p != c) {
-            if (tid == oc) {
+            if (tid == k)
 #pragma unroll
-                for (int i = 0; i < RPT; ++i)
-                    if (i == ic)
-#pragma unroll
-                        for (int j = 0; j < PNB; ++j) a[i][j] = prow[par][j];
-            }
+                for (int j = 0; j < PNB; ++j) a[0][j] = pr[j];
             if (tid == op) {
 #pragma unroll
                 for (int i = 0; i < RPT; ++i)
@@ -422,19 +421,36 @@ __global__ void __launch_bounds__(PT, 1)
                         for (int j = 0; j < PNB; ++j) a[i][j] = crow[par][j];
             }
         }
-        const double piv = prow[par][k];
+        const double piv = pr[k];
         if (piv == 0.0) {
             if (tid == 0 && *info == 0) *info = c + 1;
         } else {
+            // LAPACK dgetf2: scale by 1/piv when |piv| >= sfmin (DBL_MIN), else divide (uniform
+            // branch, so the common path carries no division)
+            if (fabs(piv) >= DBL_MIN) {
+                const double rpiv = 1.0 / piv;
 #pragma unroll
-            for (int i = 0; i < RPT; ++i) {
-                const int r = j0 + tid + i * PT;
-                if (r > c && r < n) {
-                    const double l = a[i][k] / piv;
-                    a[i][k] = l;
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = j0 + tid + i * PT;
+                    if (r > c && r < n) {
+                        const double l = a[i][k] * rpiv;
+                        a[i][k] = l;
 #pragma unroll
-                    for (int j = k + 1; j < PNB; ++j)
-                        if (j < jb) a[i][j] -= l * prow[par][j];
+                        for (int j = k + 1; j < PNB; ++j)
+                            if (j < jb) a[i][j] -= l * pr[j];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = j0 + tid + i * PT;
+                    if (r > c && r < n) {
+                        const double l = a[i][k] / piv;
+                        a[i][k] = l;
+#pragma unroll
+                        for (int j = k + 1; j < PNB; ++j)
+                            if (j < jb) a[i][j] -= l * pr[j];
+                    }
                 }
             }
         }
