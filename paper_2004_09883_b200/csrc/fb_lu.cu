@@ -525,6 +525,59 @@ __global__ void __launch_bounds__(SWAP_T)
     for (int i = 1; i < NB; ++i)
         if (i < jb) A[(int64_t)(j0 + i) * lda + col] = x[i];
 }
+// Trailing update of the look-ahead schedule: C -= A21 U12 with K = jb <= 8.  K is far too
+// small for a tensor-core tile to pay off, so this is a streaming FP64 kernel: per CTA a
+// 64 x 128 tile of C, A21 (64 x 8) and U12 (8 x 128) staged in shared memory, each thread two
+// adjacent columns (its 16 U12 values in registers) of 16 rows, coalesced 16-byte loads and
+// stores of C; per element a chain of jb FMAs (t ascending).
+constexpr int RU_TM = 64, RU_TN = 128, RU_T = 256;
+__global__ void __launch_bounds__(RU_T)
+    lu_rank_update_kernel(double* __restrict__ C, const double* __restrict__ A21, const double* __restrict__ U12,
+                          int64_t lda, int m, int nc, int jb) {
+    __shared__ double As[RU_TM][NB];
+    __shared__ double Bs[NB][RU_TN];
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    const int r0 = blockIdx.y * RU_TM, c0 = blockIdx.x * RU_TN;
+    for (int e = threadIdx.x; e < RU_TM * NB; e += RU_T) {
+        const int r = e / NB, t = e % NB;
+        As[r][t] = (r0 + r < m && t < jb) ? A21[(int64_t)(r0 + r) * lda + t] : 0.0;
+    }
+    for (int e = threadIdx.x; e < NB * RU_TN; e += RU_T) {
+        const int t = e / RU_TN, cc = e % RU_TN;
+        Bs[t][cc] = (t < jb && c0 + cc < nc) ? U12[(int64_t)t * lda + c0 + cc] : 0.0;
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    const int tx = threadIdx.x % (RU_TN / 2), ty = threadIdx.x / (RU_TN / 2);
+    const int cc = 2 * tx;
+    double b0[NB], b1[NB];
+#pragma unroll
+    for (int t = 0; t < NB; ++t) {
+        b0[t] = Bs[t][cc];
+        b1[t] = Bs[t][cc + 1];
+    }
+    const bool two = c0 + cc + 1 < nc, one = c0 + cc < nc;
+#pragma unroll 4
+    for (int r = ty; r < RU_TM; r += RU_T / (RU_TN / 2)) {
+        if (r0 + r >= m || !one) continue;
+        double* cp = C + (int64_t)(r0 + r) * lda + c0 + cc;
+        double2 cv;
+        if (two)
+            cv = *reinterpret_cast<const double2*>(cp);
+        else
+            cv = make_double2(cp[0], 0.0);
+#pragma unroll
+        for (int t = 0; t < NB; ++t) {
+            const double a = As[r][t];
+            cv.x = fma(-a, b0[t], cv.x);
+            cv.y = fma(-a, b1[t], cv.y);
+        }
+        if (two)
+            *reinterpret_cast<double2*>(cp) = cv;
+        else
+            cp[0] = cv.x;
+    }
+}
 }  // namespace lu
 
 size_t lu_ws_bytes(int64_t) { return 0; }
@@ -598,6 +651,8 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
     FB_TRY(lu_streams(&ls));
     const char* dbg_s = getenv("FB_LU_DEBUG");  // timing decomposition only (wrong results): 1 no GEMM, 2 no swap/TRSM, 4 no panel
     const int dbg = dbg_s ? atoi(dbg_s) : 0;
+    const char* rs_s = getenv("FB_LU_RANK_SIMT");  // A/B knob: 0 = DMMA GEMM for the trailing update
+    const bool rank_simt = !(rs_s && rs_s[0] == '0');
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     FB_CUDA_TRY(cudaEventRecord(ls->ev_fork, s));
     FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_fork, 0));  // w starts after everything before the call
@@ -615,15 +670,23 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
         FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_p, 0));
         const int64_t nxt = (j0 + jb < n) ? ((n - j0 - jb) < nb ? (n - j0 - jb) : nb) : 0;
         const int64_t skip_end = j0 + jb + nxt;
-        if (!(dbg & 2)) FB_TRY(lu_launch(lu::lu_swap_trsm_wide_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
-                         dim3(lu::SWAP_T), 0, ls->w, A, lda, (int)n, (int)j0, jb, (int)skip_end,
-                         (const int32_t*)ipiv));
+        if (!(dbg & 2))
+            FB_TRY(lu_launch(lu::lu_swap_trsm_wide_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
+                             dim3(lu::SWAP_T), 0, ls->w, A, lda, (int)n, (int)j0, jb, (int)skip_end,
+                             (const int32_t*)ipiv));
         const int64_t rest_r = n - j0 - jb, rest_c = n - skip_end;
         if (rest_r > 0 && rest_c > 0 && !(dbg & 1)) {
             double* A21 = A + (j0 + jb) * lda + j0;
             double* U12 = A + j0 * lda + skip_end;
             double* A22 = A + (j0 + jb) * lda + skip_end;
-            FB_TRY(gemm_f64_sub_device(rest_r, rest_c, jb, A21, lda, U12, lda, A22, lda, ls->w));
+            if (rank_simt)
+                FB_TRY(lu_launch(lu::lu_rank_update_kernel,
+                                 dim3((unsigned)((rest_c + lu::RU_TN - 1) / lu::RU_TN),
+                                      (unsigned)((rest_r + lu::RU_TM - 1) / lu::RU_TM)),
+                                 dim3(lu::RU_T), 0, ls->w, A22, (const double*)A21, (const double*)U12, lda,
+                                 (int)rest_r, (int)rest_c, jb));
+            else
+                FB_TRY(gemm_f64_sub_device(rest_r, rest_c, jb, A21, lda, U12, lda, A22, lda, ls->w));
         }
         FB_CUDA_TRY(cudaEventRecord(ls->ev_w[k & 1], ls->w));
     }
