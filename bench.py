@@ -354,6 +354,7 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                          "achieved": 3 * flops / (tk * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
                          "frac": 3 * flops / (tk * 1e-3) / 1e12 / tf32_peak,
                          "note": "achieved counts the 3 TF32 MMAs (6MNK); useful 2MNK = achieved/3",
+                         "traffic": ncu_traffic("gemm_3xtf32_kernel", "gemm_2048"),
                          "peak_source": pk["source"] + " bf16 x 0.5 (TF32/BF16 nominal ratio)"}}
         del A, B, C, ws, Ah, Al, Bh, Bl
     if want("gemm_f64_2048"):
@@ -391,8 +392,9 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
         res["lu_f64_2048"] = {"value": flops / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
                               "config": {"workload": "lu_2048_fp64_orthogonal_dct2", "survey_next": "N2",
                                          "flops": "2/3 n^3"},
-                              "note": "8-column register-resident panels + DMMA trailing updates; "
-                                      "latency-bound by the 2048 sequential pivot steps"}
+                              "note": "look-ahead: one-CTA 8-column panels (pivot search by redux.sync) overlap "
+                                      "the swap/TRSM + streaming rank-8 update of the previous step on a second "
+                                      "stream; latency-bound by the 2048 sequential pivot steps"}
         del Q, LUb
     # configs[0]: 256^2 forward + inverse
     if want("fft2d_256_fwd_inv"):

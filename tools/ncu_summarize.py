@@ -1,6 +1,6 @@
 """Summarise ncu reports into small committed text/JSON files under profiles/.
 
-usage: python tools/ncu_summarize.py REPORT.ncu-rep OUT_PREFIX
+usage: python tools/ncu_summarize.py REPORT.ncu-rep OUT_PREFIX [WORKLOAD KERNEL_SUBSTR [KEY]]
 Writes OUT_PREFIX.txt (per-kernel key metrics) and merges dram bytes per launch into
 profiles/ncu_traffic.json (keyed by workload tag inferred from the kernel name).
 """
@@ -38,6 +38,7 @@ def main():
     raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
+    scale = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "KB": 1e-3, "MB": 1.0, "GB": 1e3}
     lines = [f"# ncu --set full summary of {os.path.basename(rep)} (units: us, MB, %)"]
     traffic = {}
     for r in rows[2:]:
@@ -46,7 +47,14 @@ def main():
         vals = {}
         for k, label in KEYS:
             if k in hdr and r[hdr.index(k)] not in ("", "n/a"):
-                vals[label] = r[hdr.index(k)]
+                v = r[hdr.index(k)]
+                u = units[hdr.index(k)]
+                if label.endswith("_MB") and u in scale:  # normalise to MB whatever unit ncu chose
+                    v = "%.3f" % (float(v.replace(",", "")) * scale[u])
+                elif k == "gpu__time_duration.sum" and u in ("ns", "msecond", "usecond", "nsecond"):
+                    f = {"ns": 1e-3, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}[u]
+                    v = "%.3f" % (float(v.replace(",", "")) * f)
+                vals[label] = v
         lines.append("    " + "  ".join(f"{k}={v}" for k, v in vals.items()))
         try:
             rd = float(vals.get("dram_read_MB", "0").replace(",", ""))
@@ -60,6 +68,11 @@ def main():
     cur = json.load(open(tp)) if os.path.exists(tp) else {}
     for k, v in traffic.items():
         cur.setdefault("per_kernel_bytes", {})[k] = sum(v) / len(v)
+    if len(sys.argv) > 4:  # workload tag + kernel-name substring: mean bytes per launch of those kernels
+        tag, sub = sys.argv[3], sys.argv[4]
+        vs = [x for k, v in traffic.items() if sub in k for x in v]
+        if vs:
+            cur.setdefault(tag, {})[sys.argv[5] if len(sys.argv) > 5 else sub] = sum(vs) / len(vs)
     json.dump(cur, open(tp, "w"), indent=1)
     print("\n".join(lines))
 

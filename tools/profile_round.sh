@@ -1,6 +1,13 @@
-# Profiles committed under profiles/ (run under gpurun; one GPU).
+# Profiles committed under profiles/ (run under gpurun; one GPU).  Every ncu command below is
+# preceded by the same command run without ncu (exit 0).
 cd $GRAFT_REPO_ROOT
-CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --only gemm_f32_2048,gemm_f64_2048"
-timeout 300 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || exit 1
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r1_launches.csv $CMD > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fft_pass|gemm_3xtf32|gemm_f64|split_" -s 0 -c 8 -o gpurun_out/r1_full $CMD > gpurun_out/r1_full.log 2>&1
+R=${R:-r1}
+CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline"
+timeout 600 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || exit 1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv $CMD > /dev/null 2>&1
+HCMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras"
+timeout 600 $HCMD > /dev/null 2>&1 || exit 1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fft_pass" -s 10 -c 2 -o gpurun_out/${R}_fft2048 $HCMD > gpurun_out/${R}_fft2048.log 2>&1
+GCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --only gemm_f32_2048,gemm_f64_2048,lu_f64_2048"
+timeout 600 $GCMD > /dev/null 2>&1 || exit 1
+timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gemm_3xtf32|gemm_f64_dmma|split_|lu_panel_la|lu_rank|lu_swap" -s 3 -c 10 -o gpurun_out/${R}_gemm_lu $GCMD > gpurun_out/${R}_gemm_lu.log 2>&1
