@@ -248,6 +248,60 @@ __global__ void split_transpose_kernel(const float* __restrict__ X, int64_t rows
     }
 }
 
+// Both operand splits of fb_matmul in one launch (the two halves stream concurrently instead
+// of back to back): blocks [0, nblk_a) split A row-wise (float4 chunks, 256 columns per block
+// row segment), the rest split-transpose B in 32 x 32 tiles (as split_transpose_kernel).
+__global__ void __launch_bounds__(256)
+    split_both_kernel(const float* __restrict__ A, int64_t m, int64_t k, int64_t lda, float* __restrict__ Ah,
+                      float* __restrict__ Al, const float* __restrict__ B, int64_t n, int64_t ldb,
+                      float* __restrict__ Bh, float* __restrict__ Bl, int64_t ldo, int64_t nblk_a, int a_cblk) {
+    __shared__ float th[32][33], tl[32][33];
+    const int64_t bid = blockIdx.x;
+    if (bid < nblk_a) {
+        const int64_t r = bid / a_cblk;
+        const int64_t c4 = ((bid % a_cblk) * 256 + threadIdx.x) * 4;
+        if (c4 >= k) return;
+        const float* xr = A + r * lda;
+        float* hr = Ah + r * ldo;
+        float* lr = Al + r * ldo;
+        if (c4 + 4 <= k) {
+            const float4 x = *reinterpret_cast<const float4*>(xr + c4);
+            float4 h, l;
+            split1(x.x, h.x, l.x);
+            split1(x.y, h.y, l.y);
+            split1(x.z, h.z, l.z);
+            split1(x.w, h.w, l.w);
+            *reinterpret_cast<float4*>(hr + c4) = h;
+            *reinterpret_cast<float4*>(lr + c4) = l;
+        } else {
+            for (int64_t c = c4; c < k; ++c) split1(xr[c], hr[c], lr[c]);
+        }
+        return;
+    }
+    // B [k][n] -> hi/lo [n][ldo]
+    const int64_t tb = bid - nblk_a;
+    const int64_t tiles_c = (n + 31) / 32;
+    const int64_t r0 = (tb / tiles_c) * 32, c0 = (tb % tiles_c) * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+        const int64_t r = r0 + ty + j, c = c0 + tx;
+        const float x = (r < k && c < n) ? B[r * ldb + c] : 0.f;
+        const float hf = __uint_as_float(ptx::f32_to_tf32_rna(x));
+        th[ty + j][tx] = hf;
+        tl[ty + j][tx] = __uint_as_float(ptx::f32_to_tf32_rna(x - hf));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 32; j += 8) {
+        const int64_t c = c0 + ty + j, r = r0 + tx;
+        if (c < n && r < k) {
+            Bh[c * ldo + r] = th[tx][ty + j];
+            Bl[c * ldo + r] = tl[tx][ty + j];
+        }
+    }
+}
+
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
     const int per_group = GROUP_M * tiles_n;
     const int grp = tile / per_group;
@@ -477,6 +531,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
+    ptx::pdl_wait();  // PDL: the split kernel's outputs are complete (setup above overlapped it)
 
     if (warp == 0) {
         if (lane == 0) {
@@ -691,8 +746,22 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
     float* Al = Ah + m * kp;
     float* Bh = Al + m * kp;
     float* Bl = Bh + n * kp;
-    FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
-    FB_TRY(tf32_split_device(1, k, n, (const float*)B, ldb, Bh, Bl, kp, st, s));
+    const char* sk = getenv("FB_GEMM_SPLIT2");  // A/B knob: 1 = two split launches
+    if (sk && sk[0] == '1') {
+        FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
+        FB_TRY(tf32_split_device(1, k, n, (const float*)B, ldb, Bh, Bl, kp, st, s));
+    } else {
+        const int a_cblk = (int)((((k + 3) / 4) + 255) / 256);
+        const int64_t nblk_a = m * a_cblk;
+        const int64_t nblk_b = ((k + 31) / 32) * ((n + 31) / 32);
+        if (nblk_a + nblk_b > INT32_MAX) {
+            set_error("split grid too large");
+            return FB_ERR_UNSUPPORTED_SIZE;
+        }
+        tf32::split_both_kernel<<<(unsigned)(nblk_a + nblk_b), 256, 0, s>>>(
+            (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a, a_cblk);
+        FB_LAUNCH_CHECK("split_both_kernel");
+    }
     return gemm_3xtf32_presplit_device(m, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C, ldc, s);
 }
 
@@ -743,8 +812,18 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
             set_error("too many tiles");
             return FB_ERR_UNSUPPORTED_SIZE;
         }
-        tf32::pair::gemm_3xtf32_pair_kernel<<<(unsigned)(2 * tiles), tf32::pair::NUM_THREADS, tf32::pair::SMEM, s>>>(
-            mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, ldc, tiles_m, tiles_n);
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3((unsigned)(2 * tiles));
+        cfg.blockDim = dim3(tf32::pair::NUM_THREADS);
+        cfg.dynamicSmemBytes = tf32::pair::SMEM;
+        cfg.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[0].val.programmaticStreamSerializationAllowed = 1;
+        cfg.attrs = attr;
+        cfg.numAttrs = 1;
+        FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf32::pair::gemm_3xtf32_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m,
+                                       (int)n, (int)k, ldc, tiles_m, tiles_n));
         FB_LAUNCH_CHECK("gemm_3xtf32_pair_kernel");
         return FB_OK;
     }
