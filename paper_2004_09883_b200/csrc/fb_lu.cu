@@ -12,7 +12,9 @@
 //   2. lu_swap_trsm_kernel  the panel's swaps applied, in order, to every other column, then
 //                        U12 = L11^-1 A12 (unit lower 8x8) for the columns right of the panel;
 //   4. A22 -= A21 U12    the DMMA GEMM with a subtracting epilogue (fb_gemm.cu).
+#include <cuda.h>
 #include <float.h>
+#include <string.h>
 
 #include "fb_common.cuh"
 #include "fb_ptx.cuh"
@@ -219,21 +221,131 @@ __device__ __forceinline__ int lu_pidx(int r, int j) {
     return r * PNB + 2 * c + (j & 1);
 }
 
+// The PNB pivot steps of a panel held in registers (thread tid owns rows j0 + tid + i*PT):
+// pivot search, swap and rank-1 updates (shared by the cp.async and TMA panel kernels).
 template <int PT, int RPT, int PNB>
-__global__ void __launch_bounds__(PT, 1)
-    lu_panel_la_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int has_prev,
-                       int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
+__device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid, int j0, int jb, int n,
+                                                 int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
     constexpr int NW = PT / 32;
-    constexpr int CH = PNB / 2;
     __shared__ double red_row[2][NW][PNB];  // each warp's candidate row
     __shared__ unsigned long long red_k[2][NW];
     __shared__ int red_r[2][NW];
     __shared__ double crow[2][PNB];
+    const int lane = tid & 31, warp = tid >> 5;
+#pragma unroll
+    for (int k = 0; k < PNB; ++k) {
+        if (k >= jb) break;
+        const int par = k & 1;
+        const int c = j0 + k;
+        double bv = -1.0;
+        int br = INT_MAX, bi = 0;
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int r = j0 + tid + i * PT;
+            const double v = fabs(a[i][k]);
+            if (r >= c && r < n && v > bv) {
+                bv = v;
+                br = r;
+                bi = i;
+            }
+        }
+        // pivot = (max |a|, then smallest row): |a| >= 0 orders like its IEEE bit pattern, so
+        // the warp and cross-warp reductions are three redux.sync each (max hi word, max lo
+        // word among the max-hi lanes, min row among the max lanes); "no candidate" is key 0
+        // with row INT_MAX, which a real zero pivot candidate beats on the row.  The lane that
+        // holds its warp's candidate publishes the candidate's whole row, and the owner of row c
+        // (thread k) publishes row c, before the one barrier of the column: afterwards every
+        // thread reads the pivot row from the winning warp's slot, so no second barrier.
+        unsigned long long key = bv >= 0.0 ? (unsigned long long)__double_as_longlong(bv) : 0ull;
+        unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
+        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
+        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? br : INT_MAX));
+        if (br == wr && wr != INT_MAX) {
+#pragma unroll
+            for (int i = 0; i < RPT; ++i)
+                if (i == bi)
+#pragma unroll
+                    for (int j = 0; j < PNB; ++j) red_row[par][warp][j] = a[i][j];
+        }
+        if (lane == 0) {
+            red_k[par][warp] = ((unsigned long long)mhi << 32) | mlo;
+            red_r[par][warp] = wr;
+        }
+        if (tid == k)
+#pragma unroll
+            for (int j = 0; j < PNB; ++j) crow[par][j] = a[0][j];  // row c = j0 + k is thread k's row 0
+        __syncthreads();
+        key = (lane < NW) ? red_k[par][lane] : 0ull;
+        const int rw = (lane < NW) ? red_r[par][lane] : INT_MAX;
+        khi = (unsigned)(key >> 32);
+        klo = (unsigned)key;
+        mhi = __reduce_max_sync(0xffffffffu, khi);
+        mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
+        const int p = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? rw : INT_MAX));
+        if (tid == 0) ipiv[c] = p;
+        const int op = (p - j0) % PT, ip = (p - j0) / PT;
+        double pr[PNB];
+#pragma unroll
+        for (int j = 0; j < PNB; ++j) pr[j] = red_row[par][op >> 5][j];
+        if (p != c) {
+            if (tid == k)
+#pragma unroll
+                for (int j = 0; j < PNB; ++j) a[0][j] = pr[j];
+            if (tid == op) {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i)
+                    if (i == ip)
+#pragma unroll
+                        for (int j = 0; j < PNB; ++j) a[i][j] = crow[par][j];
+            }
+        }
+        const double piv = pr[k];
+        if (piv == 0.0) {
+            if (tid == 0 && *info == 0) *info = c + 1;
+        } else {
+            // LAPACK dgetf2: scale by 1/piv when |piv| >= sfmin (DBL_MIN), else divide (uniform
+            // branch, so the common path carries no division)
+            if (fabs(piv) >= DBL_MIN) {
+                const double rpiv = 1.0 / piv;
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = j0 + tid + i * PT;
+                    if (r > c && r < n) {
+                        const double l = a[i][k] * rpiv;
+                        a[i][k] = l;
+#pragma unroll
+                        for (int j = k + 1; j < PNB; ++j)
+                            if (j < jb) a[i][j] -= l * pr[j];
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int i = 0; i < RPT; ++i) {
+                    const int r = j0 + tid + i * PT;
+                    if (r > c && r < n) {
+                        const double l = a[i][k] / piv;
+                        a[i][k] = l;
+#pragma unroll
+                        for (int j = k + 1; j < PNB; ++j)
+                            if (j < jb) a[i][j] -= l * pr[j];
+                    }
+                }
+            }
+        }
+    }
+}
+
+template <int PT, int RPT, int PNB>
+__global__ void __launch_bounds__(PT, 1)
+    lu_panel_la_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int has_prev,
+                       int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
+    constexpr int CH = PNB / 2;
     __shared__ double L11[PNB][PNB];
     __shared__ double Us[PNB][PNB];  // U12 rows of this panel's columns
     __shared__ int pv[PNB];
     extern __shared__ __align__(16) double smem_lu[];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x;
     asm volatile("griddepcontrol.wait;" ::: "memory");
 #ifdef FB_LU_TIMING
     long long tt[6];
@@ -353,108 +465,7 @@ __global__ void __launch_bounds__(PT, 1)
 #ifdef FB_LU_TIMING
     tt[3] = clock64();
 #endif
-#pragma unroll
-    for (int k = 0; k < PNB; ++k) {
-        if (k >= jb) break;
-        const int par = k & 1;
-        const int c = j0 + k;
-        double bv = -1.0;
-        int br = INT_MAX, bi = 0;
-#pragma unroll
-        for (int i = 0; i < RPT; ++i) {
-            const int r = j0 + tid + i * PT;
-            const double v = fabs(a[i][k]);
-            if (r >= c && r < n && v > bv) {
-                bv = v;
-                br = r;
-                bi = i;
-            }
-        }
-        // pivot = (max |a|, then smallest row): |a| >= 0 orders like its IEEE bit pattern, so
-        // the warp and cross-warp reductions are three redux.sync each (max hi word, max lo
-        // word among the max-hi lanes, min row among the max lanes); "no candidate" is key 0
-        // with row INT_MAX, which a real zero pivot candidate beats on the row.  The lane that
-        // holds its warp's candidate publishes the candidate's whole row, and the owner of row c
-        // (thread k) publishes row c, before the one barrier of the column: afterwards every
-        // thread reads the pivot row from the winning warp's slot, so no second barrier.
-        unsigned long long key = bv >= 0.0 ? (unsigned long long)__double_as_longlong(bv) : 0ull;
-        unsigned khi = (unsigned)(key >> 32), klo = (unsigned)key;
-        unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
-        unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
-        const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? br : INT_MAX));
-        if (br == wr && wr != INT_MAX) {
-#pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                if (i == bi)
-#pragma unroll
-                    for (int j = 0; j < PNB; ++j) red_row[par][warp][j] = a[i][j];
-        }
-        if (lane == 0) {
-            red_k[par][warp] = ((unsigned long long)mhi << 32) | mlo;
-            red_r[par][warp] = wr;
-        }
-        if (tid == k)
-#pragma unroll
-            for (int j = 0; j < PNB; ++j) crow[par][j] = a[0][j];  // row c = j0 + k is thread k's row 0
-        __syncthreads();
-        key = (lane < NW) ? red_k[par][lane] : 0ull;
-        const int rw = (lane < NW) ? red_r[par][lane] : INT_MAX;
-        khi = (unsigned)(key >> 32);
-        klo = (unsigned)key;
-        mhi = __reduce_max_sync(0xffffffffu, khi);
-        mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
-        const int p = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? rw : INT_MAX));
-        if (tid == 0) ipiv[c] = p;
-        const int op = (p - j0) % PT, ip = (p - j0) / PT;
-        double pr[PNB];
-#pragma unroll
-        for (int j = 0; j < PNB; ++j) pr[j] = red_row[par][op >> 5][j];
-        if (p != c) {
-            if (tid == k)
-#pragma unroll
-                for (int j = 0; j < PNB; ++j) a[0][j] = pr[j];
-            if (tid == op) {
-#pragma unroll
-                for (int i = 0; i < RPT; ++i)
-                    if (i == ip)
-#pragma unroll
-                        for (int j = 0; j < PNB; ++j) a[i][j] = crow[par][j];
-            }
-        }
-        const double piv = pr[k];
-        if (piv == 0.0) {
-            if (tid == 0 && *info == 0) *info = c + 1;
-        } else {
-            // LAPACK dgetf2: scale by 1/piv when |piv| >= sfmin (DBL_MIN), else divide (uniform
-            // branch, so the common path carries no division)
-            if (fabs(piv) >= DBL_MIN) {
-                const double rpiv = 1.0 / piv;
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                    const int r = j0 + tid + i * PT;
-                    if (r > c && r < n) {
-                        const double l = a[i][k] * rpiv;
-                        a[i][k] = l;
-#pragma unroll
-                        for (int j = k + 1; j < PNB; ++j)
-                            if (j < jb) a[i][j] -= l * pr[j];
-                    }
-                }
-            } else {
-#pragma unroll
-                for (int i = 0; i < RPT; ++i) {
-                    const int r = j0 + tid + i * PT;
-                    if (r > c && r < n) {
-                        const double l = a[i][k] / piv;
-                        a[i][k] = l;
-#pragma unroll
-                        for (int j = k + 1; j < PNB; ++j)
-                            if (j < jb) a[i][j] -= l * pr[j];
-                    }
-                }
-            }
-        }
-    }
+    lu_panel_columns<PT, RPT, PNB>(a, tid, j0, jb, n, ipiv, info);
 #ifdef FB_LU_TIMING
     tt[4] = clock64();
 #endif
@@ -483,6 +494,179 @@ __global__ void __launch_bounds__(PT, 1)
     if (tid == 0 && (j0 == 80 || j0 == 1024 || j0 == 1600))
         printf("LU_TIMING j0=%d stage=%lld prevprep=%lld update=%lld columns=%lld writeback=%lld total=%lld\n", j0,
                tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[5] - tt[0]);
+#endif
+}
+
+// TMA form of lu_panel_la_kernel: the panel rows [r0, n), the L21 batches and the write-back
+// move as 2D tensor boxes of PNB columns x 256 rows (one thread issues them; the TMA engine's
+// 64-byte (PNB = 8) / 32-byte (PNB = 4) swizzle is exactly the XOR layout lu_pidx reads), so
+// the copies cost no LSU issue slots and the write-back drains while the CTA exits.
+// Out-of-range rows / columns are zero-filled on load and clipped on store.
+constexpr int LU_BOXR = 256;
+template <int PT, int RPT, int PNB>
+__global__ void __launch_bounds__(PT, 1)
+    lu_panel_tma_kernel(double* __restrict__ A, int64_t lda, int n, int j0, int jb, int has_prev,
+                        int32_t* __restrict__ ipiv, int32_t* __restrict__ info,
+                        const __grid_constant__ CUtensorMap tmA) {
+    static_assert(PT % LU_BOXR == 0, "L21 batches are whole boxes");
+    __shared__ double L11[PNB][PNB];
+    __shared__ double Us[PNB][PNB];
+    __shared__ int pv[PNB];
+    __shared__ __align__(8) uint64_t bars[3];
+    extern __shared__ __align__(16) double smem_lu[];
+    const int tid = threadIdx.x;
+    const int jp = j0 - PNB;
+    const int r0 = has_prev ? jp : j0;
+    const int mr = n - r0;
+    const int m = n - j0;
+    const int off = j0 - r0;
+    // [mr][PNB] swizzled, 1024-aligned (the swizzle pattern follows the smem address bits)
+    double* P = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(smem_lu) + 1023) & ~uintptr_t(1023));
+    // whole boxes land in P (out-of-range rows as zeros), so it spans ceil(mr / 256) boxes
+    double* Lb = P + ((mr + LU_BOXR - 1) / LU_BOXR) * LU_BOXR * PNB;  // [2][PT][PNB] swizzled
+    const uint32_t bar_p = ptx::smem_u32(&bars[0]);
+    auto bar_l = [&](int b) { return ptx::smem_u32(&bars[1 + b]); };
+    constexpr uint32_t BOX_BYTES = LU_BOXR * PNB * sizeof(double);
+    auto load_l = [&](int i, int b) {  // L21 rows j0 + i*PT + [0, PT), columns jp.. (thread 0)
+        ptx::mbar_arrive_expect_tx(bar_l(b), (uint32_t)(PT / LU_BOXR) * BOX_BYTES);
+        for (int q = 0; q < PT / LU_BOXR; ++q)
+            ptx::tma_load_2d(ptx::smem_u32(Lb + (b * PT + q * LU_BOXR) * PNB), &tmA, bar_l(b), jp,
+                             j0 + i * PT + q * LU_BOXR);
+    };
+    if (tid == 0) {
+        ptx::mbar_init(bar_p, 1);
+        ptx::mbar_init(bar_l(0), 1);
+        ptx::mbar_init(bar_l(1), 1);
+        ptx::fence_mbar_init();
+        ptx::tma_prefetch_desc(&tmA);
+    }
+    __syncthreads();
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+#ifdef FB_LU_TIMING
+    long long tt[6];
+    tt[0] = clock64();
+#endif
+    if (tid == 0) {
+        const int nbox = (mr + LU_BOXR - 1) / LU_BOXR;
+        ptx::mbar_arrive_expect_tx(bar_p, (uint32_t)nbox * BOX_BYTES);
+        for (int q = 0; q < nbox; ++q)
+            ptx::tma_load_2d(ptx::smem_u32(P + q * LU_BOXR * PNB), &tmA, bar_p, j0, r0 + q * LU_BOXR);
+        if (has_prev) {
+            load_l(0, 0);
+            if (RPT > 1) load_l(1, 1);
+        }
+    }
+    if (has_prev) {
+        if (tid < PNB * PNB) {
+            const int i = tid / PNB, k = tid % PNB;
+            L11[i][k] = A[(int64_t)(jp + i) * lda + jp + k];
+        }
+        if (tid < PNB) pv[tid] = ipiv[jp + tid];
+    }
+    ptx::mbar_wait(bar_p, 0);
+    __syncthreads();
+#ifdef FB_LU_TIMING
+    tt[1] = clock64();
+#endif
+    if (has_prev) {
+        if (tid < PNB) {  // column tid: previous swaps in order, then x = L11^-1 x on rows jp..
+            const int j = tid;
+#pragma unroll 1
+            for (int t = 0; t < PNB; ++t) {
+                const int q = pv[t] - r0;
+                if (q != t) {
+                    const double tmp = P[lu_pidx<PNB>(t, j)];
+                    P[lu_pidx<PNB>(t, j)] = P[lu_pidx<PNB>(q, j)];
+                    P[lu_pidx<PNB>(q, j)] = tmp;
+                }
+            }
+            double x[PNB];
+#pragma unroll
+            for (int i = 0; i < PNB; ++i) x[i] = P[lu_pidx<PNB>(i, j)];
+#pragma unroll
+            for (int i = 1; i < PNB; ++i)
+#pragma unroll
+                for (int k = 0; k < i; ++k) x[i] -= L11[i][k] * x[k];
+#pragma unroll
+            for (int i = 0; i < PNB; ++i) {
+                Us[i][j] = x[i];
+                P[lu_pidx<PNB>(i, j)] = x[i];  // U12 rows leave with the write-back
+            }
+        }
+        __syncthreads();
+    }
+    double a[RPT][PNB];
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int rr = tid + i * PT;
+#pragma unroll
+        for (int c = 0; c < PNB / 2; ++c) {
+            double2 v = make_double2(0.0, 0.0);
+            if (rr < m) v = *reinterpret_cast<const double2*>(P + lu_pidx<PNB>(off + rr, 2 * c));
+            a[i][2 * c] = v.x;
+            a[i][2 * c + 1] = v.y;
+        }
+    }
+#ifdef FB_LU_TIMING
+    tt[2] = clock64();
+#endif
+    if (has_prev) {  // A[r][j0 + j] -= sum_t L21[r][t] U12[t][j]
+#pragma unroll
+        for (int i = 0; i < RPT; ++i) {
+            const int b = i & 1;
+            ptx::mbar_wait(bar_l(b), (uint32_t)(i >> 1) & 1u);
+            double l[PNB];
+#pragma unroll
+            for (int c = 0; c < PNB / 2; ++c) {
+                const double2 v = *reinterpret_cast<const double2*>(Lb + b * PT * PNB + lu_pidx<PNB>(tid, 2 * c));
+                l[2 * c] = v.x;
+                l[2 * c + 1] = v.y;
+            }
+#pragma unroll
+            for (int j = 0; j < PNB; ++j) {
+                double acc = 0.0;
+#pragma unroll
+                for (int t = 0; t < PNB; ++t) acc = fma(l[t], Us[t][j], acc);
+                a[i][j] -= acc;
+            }
+            if (i + 2 < RPT) {  // refill buffer b with batch i + 2 once every thread has read it
+                ptx::fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0) load_l(i + 2, b);
+            }
+        }
+    }
+#ifdef FB_LU_TIMING
+    tt[3] = clock64();
+#endif
+    lu_panel_columns<PT, RPT, PNB>(a, tid, j0, jb, n, ipiv, info);
+#ifdef FB_LU_TIMING
+    tt[4] = clock64();
+#endif
+    // write back rows [r0, n) (U12 rows + this panel): registers -> P -> TMA stores
+#pragma unroll
+    for (int i = 0; i < RPT; ++i) {
+        const int rr = tid + i * PT;
+        if (rr < m)
+#pragma unroll
+            for (int c = 0; c < PNB / 2; ++c)
+                *reinterpret_cast<double2*>(P + lu_pidx<PNB>(off + rr, 2 * c)) =
+                    make_double2(a[i][2 * c], a[i][2 * c + 1]);
+    }
+    ptx::fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+        const int nbox = (mr + LU_BOXR - 1) / LU_BOXR;
+        for (int q = 0; q < nbox; ++q) ptx::tma_store_2d(&tmA, ptx::smem_u32(P + q * LU_BOXR * PNB), j0, r0 + q * LU_BOXR);
+        ptx::bulk_commit();
+        ptx::bulk_wait0();
+    }
+#ifdef FB_LU_TIMING
+    __syncthreads();
+    tt[5] = clock64();
+    if (tid == 0 && (j0 == 80 || j0 == 1024 || j0 == 1600))
+        printf("LU_TIMING tma j0=%d stage=%lld prevprep=%lld update=%lld columns=%lld writeback=%lld total=%lld\n",
+               j0, tt[1] - tt[0], tt[2] - tt[1], tt[3] - tt[2], tt[4] - tt[3], tt[5] - tt[4], tt[5] - tt[0]);
 #endif
 }
 
@@ -638,21 +822,61 @@ static fb_status lu_streams(LuStreams** out) {
     return FB_OK;
 }
 
+typedef CUresult (*EncodeTiledFnLU)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                    const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                    CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+// A as a 2D FP64 tensor {n columns, n rows}, box {PNB columns, 256 rows}, swizzled like lu_pidx
+static fb_status lu_tensor_map(CUtensorMap* m, double* A, int64_t n, int64_t lda, int pnb) {
+    static EncodeTiledFnLU enc = nullptr;
+    if (!enc) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess) {
+            set_error("cuTensorMapEncodeTiled unavailable from the driver");
+            return FB_ERR_CUDA;
+        }
+        enc = (EncodeTiledFnLU)f;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)n, (cuuint64_t)n};
+    cuuint64_t strides[1] = {(cuuint64_t)(lda * 8)};
+    cuuint32_t box[2] = {(cuuint32_t)pnb, (cuuint32_t)lu::LU_BOXR};
+    cuuint32_t estr[2] = {1u, 1u};
+    const CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, A, dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           pnb == 8 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) {
+        set_error("cuTensorMapEncodeTiled failed (%d) for the LU panel map", (int)r);
+        return FB_ERR_CUDA;
+    }
+    return FB_OK;
+}
+
 template <int PT, int RPT, int PNB>
 static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
     constexpr int nb = PNB;
     auto panel = lu::lu_panel_la_kernel<PT, RPT, PNB>;
+    auto panel_tma = lu::lu_panel_tma_kernel<PT, RPT, PNB>;
     static bool attr = false;
     if (!attr) {
         FB_CUDA_TRY(cudaFuncSetAttribute(panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        FB_CUDA_TRY(cudaFuncSetAttribute(panel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         attr = true;
     }
+    const char* tk = getenv("FB_LU_TMA");  // A/B knob: 0 = cp.async panel kernel
+    const bool use_tma = !(tk && tk[0] == '0') && (lda * 8) % 16 == 0 && ((uintptr_t)A & 15) == 0;
+    CUtensorMap tmA;
+    memset(&tmA, 0, sizeof(tmA));
+    if (use_tma) FB_TRY(lu_tensor_map(&tmA, A, n, lda, PNB));
     LuStreams* ls;
     FB_TRY(lu_streams(&ls));
     const char* dbg_s = getenv("FB_LU_DEBUG");  // timing decomposition only (wrong results): 1 no GEMM, 2 no swap/TRSM, 4 no panel
     const int dbg = dbg_s ? atoi(dbg_s) : 0;
     const char* rs_s = getenv("FB_LU_RANK_SIMT");  // A/B knob: 0 = DMMA GEMM for the trailing update
     const bool rank_simt = !(rs_s && rs_s[0] == '0');
+    const char* ser = getenv("FB_LU_SERIAL");  // debug knob: run the wide parts on the caller's stream
+    cudaStream_t wst = (ser && ser[0] == '1') ? s : ls->w;
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     FB_CUDA_TRY(cudaEventRecord(ls->ev_fork, s));
     FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_fork, 0));  // w starts after everything before the call
@@ -663,8 +887,18 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
         if (k >= 2) FB_CUDA_TRY(cudaStreamWaitEvent(s, ls->ev_w[k & 1], 0));  // wide_{k-2}
         const int64_t r0 = has_prev ? j0 - nb : j0;
         const size_t smem = (size_t)(n - r0) * PNB * sizeof(double) + (size_t)2 * PT * PNB * sizeof(double);
-        if (!(dbg & 4))
-            FB_TRY(lu_launch(panel, dim3(1), dim3(PT), smem, s, A, lda, (int)n, (int)j0, jb, has_prev, ipiv, info));
+        if (!(dbg & 4)) {
+            if (use_tma) {
+                const size_t smem_tma = (size_t)((n - r0 + lu::LU_BOXR - 1) / lu::LU_BOXR) * lu::LU_BOXR * PNB *
+                                            sizeof(double) +
+                                        (size_t)2 * PT * PNB * sizeof(double) + 1024;
+                FB_TRY(lu_launch(panel_tma, dim3(1), dim3(PT), smem_tma, s, A, lda, (int)n, (int)j0, jb, has_prev,
+                                 ipiv, info, tmA));
+            }
+            else
+                FB_TRY(lu_launch(panel, dim3(1), dim3(PT), smem, s, A, lda, (int)n, (int)j0, jb, has_prev, ipiv,
+                                 info));
+        }
         FB_CUDA_TRY(cudaEventRecord(ls->ev_p, s));
         // wide part of this step: everything except this panel and the next one
         FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_p, 0));
@@ -672,7 +906,7 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
         const int64_t skip_end = j0 + jb + nxt;
         if (!(dbg & 2))
             FB_TRY(lu_launch(lu::lu_swap_trsm_wide_kernel, dim3((unsigned)((n + lu::SWAP_T - 1) / lu::SWAP_T)),
-                             dim3(lu::SWAP_T), 0, ls->w, A, lda, (int)n, (int)j0, jb, (int)skip_end,
+                             dim3(lu::SWAP_T), 0, wst, A, lda, (int)n, (int)j0, jb, (int)skip_end,
                              (const int32_t*)ipiv));
         const int64_t rest_r = n - j0 - jb, rest_c = n - skip_end;
         if (rest_r > 0 && rest_c > 0 && !(dbg & 1)) {
@@ -683,12 +917,12 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
                 FB_TRY(lu_launch(lu::lu_rank_update_kernel,
                                  dim3((unsigned)((rest_c + lu::RU_TN - 1) / lu::RU_TN),
                                       (unsigned)((rest_r + lu::RU_TM - 1) / lu::RU_TM)),
-                                 dim3(lu::RU_T), 0, ls->w, A22, (const double*)A21, (const double*)U12, lda,
+                                 dim3(lu::RU_T), 0, wst, A22, (const double*)A21, (const double*)U12, lda,
                                  (int)rest_r, (int)rest_c, jb));
             else
-                FB_TRY(gemm_f64_sub_device(rest_r, rest_c, jb, A21, lda, U12, lda, A22, lda, ls->w));
+                FB_TRY(gemm_f64_sub_device(rest_r, rest_c, jb, A21, lda, U12, lda, A22, lda, wst));
         }
-        FB_CUDA_TRY(cudaEventRecord(ls->ev_w[k & 1], ls->w));
+        FB_CUDA_TRY(cudaEventRecord(ls->ev_w[k & 1], wst));
     }
     const int klast = (int)((n - 1) / nb);
     FB_CUDA_TRY(cudaStreamWaitEvent(s, ls->ev_w[klast & 1], 0));  // join: the last wide part
