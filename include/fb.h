@@ -75,7 +75,9 @@ fb_status fb_init(int device);
  * x and y: device pointers, 16-byte aligned, n0*n1*8 bytes each; x == y (in place) is
  * allowed, partial overlap is FB_ERR_INVALID_VALUE.
  * ws: device workspace of fb_fft2d_workspace_bytes(n0, n1) bytes (may be NULL when that
- * is 0 -- every n0 <= 4096).  Not read before written; contents undefined afterwards.
+ * is 0: n0 < 512 or n0 == 4096; the 2 x n0/2 column split for 512 <= n0 <= 2048 and the
+ * four-step split for n0 > 4096 use n0*n1*8 bytes).  Not read before written; contents
+ * undefined afterwards.
  * Accuracy (north_star): rel-L2 <= 1e-5 * log2(n0 n1) vs the exact DFT; internal gate
  * 5e-7 (reading R6). */
 size_t fb_fft2d_workspace_bytes(int64_t n0, int64_t n1);
@@ -83,6 +85,15 @@ fb_status fb_fft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, siz
                    void* stream);
 fb_status fb_ifft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, size_t ws_bytes,
                     void* stream);
+
+/* Batched 1D transform: `batch` independent lines of length n, line b at
+ * x + b*n complex64 elements (contiguous rows of a batch x n array):
+ *   Y[b][k] = sum_t X[b][t] exp(-2 pi i k t / n)   (unscaled);  fb_ifft1d_batched: +1, 1/n.
+ * One pass of the same line kernels as fb_fft2d.  n a power of two <= 16384, batch >= 1,
+ * x and y 16-byte aligned, in place allowed (partial overlap: FB_ERR_INVALID_VALUE); no
+ * workspace.  Accuracy as fb_fft2d with N = n. */
+fb_status fb_fft1d_batched(const void* x, void* y, int64_t n, int64_t batch, void* stream);
+fb_status fb_ifft1d_batched(const void* x, void* y, int64_t n, int64_t batch, void* stream);
 
 /* ------------------------------------------------------------------ matrix block
  * C[m][n] = A[m][k] * B[k][n]  (row-major, leading dimensions in ELEMENTS, C overwritten).

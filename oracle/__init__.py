@@ -40,6 +40,7 @@ def lib():
         vp, i64, ci, dp = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p
         L.oracle_dft2d.argtypes = [vp, ci, dp, i64, i64, ci, ci]
         L.oracle_dft2d_bruteforce.argtypes = [vp, ci, dp, i64, i64, ci]
+        L.oracle_dft1d_rows.argtypes = [vp, ci, dp, i64, i64, ci, ci]
         L.oracle_dft2d_col.argtypes = [vp, ci, i64, i64, i64, ci, dp, ci]
         L.oracle_dft2d_row.argtypes = [vp, ci, i64, i64, i64, ci, dp, ci]
         L.oracle_matmul.argtypes = [i64, i64, i64, vp, i64, vp, i64, ci, dp, i64, ci]
@@ -47,7 +48,7 @@ def lib():
         L.oracle_matmul_cols.argtypes = [i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, dp, ci]
         L.oracle_threads.argtypes = [ci]
         L.oracle_lu.argtypes = [i64, vp, i64, vp, ci]
-        for f in ("oracle_dft2d", "oracle_dft2d_bruteforce", "oracle_dft2d_col",
+        for f in ("oracle_dft2d", "oracle_dft2d_bruteforce", "oracle_dft1d_rows", "oracle_dft2d_col",
                   "oracle_dft2d_row", "oracle_matmul", "oracle_matmul_rows",
                   "oracle_matmul_cols", "oracle_threads", "oracle_lu"):
             getattr(L, f).restype = ci
@@ -86,6 +87,16 @@ def dft2d(x, inverse: bool = False, nthreads: int = 0) -> np.ndarray:
     X = np.empty((n0, n1), dtype=np.complex128)
     _check(lib().oracle_dft2d(x.ctypes.data, t, X.ctypes.data, n0, n1,
                               1 if inverse else -1, nthreads), "oracle_dft2d")
+    return X
+
+
+def dft1d_rows(x, inverse: bool = False, nthreads: int = 0) -> np.ndarray:
+    """1D DFT definition of every row of x[batch][n] (inverse scales by 1/n)."""
+    x, t = _cin(x)
+    b, n = x.shape
+    X = np.empty((b, n), dtype=np.complex128)
+    _check(lib().oracle_dft1d_rows(x.ctypes.data, t, X.ctypes.data, b, n, 1 if inverse else -1, nthreads),
+           "oracle_dft1d_rows")
     return X
 
 

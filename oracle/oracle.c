@@ -130,6 +130,29 @@ int oracle_dft2d(const void* x, int in_type, double* X, int64_t n0, int64_t n1, 
     return 0;
 }
 
+int oracle_dft1d_rows(const void* x, int in_type, double* X, int64_t batch, int64_t n, int sign,
+                      int threads) {
+    if (batch <= 0 || n <= 0 || (sign != -1 && sign != 1)) return 1;
+    double* w = make_twiddles(n, sign);
+    if (!w) return 2;
+    int nt = oracle_threads(threads);
+    (void)nt;
+    const double scale = (sign == 1) ? 1.0 / (double)n : 1.0;
+#pragma omp parallel num_threads(nt)
+    {
+        double* row = (double*)malloc(sizeof(double) * 2 * (size_t)n);
+#pragma omp for schedule(dynamic, 1)
+        for (int64_t b = 0; b < batch; ++b) {
+            for (int64_t t = 0; t < n; ++t) load_c(x, in_type, b * n + t, &row[2 * t], &row[2 * t + 1]);
+            dft1d(row, 1, X + 2 * b * n, 1, n, w);
+            for (int64_t k = 0; k < 2 * n; ++k) X[2 * b * n + k] *= scale;
+        }
+        free(row);
+    }
+    free(w);
+    return 0;
+}
+
 int oracle_dft2d_bruteforce(const void* x, int in_type, double* X, int64_t n0, int64_t n1,
                             int sign) {
     if (n0 <= 0 || n1 <= 0 || (sign != -1 && sign != 1)) return 1;

@@ -46,6 +46,13 @@ int oracle_dft2d(const void* x, int in_type, double* X, int64_t n0, int64_t n1,
 int oracle_dft2d_bruteforce(const void* x, int in_type, double* X, int64_t n0, int64_t n1,
                             int sign);
 
+/* Batched 1D DFT (the 1D transform the paper's Fourier block applies per
+ * signal): X[b][k] = sum_t x[b][t] exp(sign 2 pi i k t / n) for each of `batch`
+ * contiguous lines of length n (inverse, sign +1: times 1/n).  Same O(n^2) definition and
+ * twiddles as one stage of oracle_dft2d. */
+int oracle_dft1d_rows(const void* x, int in_type, double* X, int64_t batch, int64_t n, int sign,
+                      int threads);
+
 /* One output column X[:, k1] (n0 complex values) of the 2D DFT of x[n0][n1]. */
 int oracle_dft2d_col(const void* x, int in_type, int64_t n0, int64_t n1, int64_t k1,
                      int sign, double* out, int threads);

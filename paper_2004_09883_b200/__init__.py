@@ -27,7 +27,7 @@ _STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_VALUE", 2: "FB_ERR_UNSUPPORTED_SIZE", 
 # every symbol include/fb.h declares (checked by tests/test_abi.py)
 EXPORTS = [
     "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_init",
-    "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d",
+    "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d", "fb_fft1d_batched", "fb_ifft1d_batched",
     "fb_matmul_workspace_bytes", "fb_matmul", "fb_tf32_split", "fb_matmul_3xtf32_presplit",
     "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
@@ -65,6 +65,8 @@ def lib() -> ctypes.CDLL:
         "fb_fft2d_workspace_bytes": ([i64, i64], sz),
         "fb_fft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
         "fb_ifft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_fft1d_batched": ([vp, vp, i64, i64, vp], ci),
+        "fb_ifft1d_batched": ([vp, vp, i64, i64, vp], ci),
         "fb_matmul_workspace_bytes": ([ci, i64, i64, i64], sz),
         "fb_matmul": ([ci, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], ci),
         "fb_tf32_split": ([ci, i64, i64, vp, i64, vp, vp, i64, vp], ci),
@@ -164,6 +166,17 @@ def fft2d(x: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = Fals
     n0, n1 = x.shape
     ws = _workspace(lib().fb_fft2d_workspace_bytes(n0, n1), x.device)
     (fb_ifft2d if inverse else fb_fft2d)(x, out, ws, stream)
+    return out
+
+
+def fft1d(x: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = False, stream=None) -> torch.Tensor:
+    """1D DFT of every row of a [batch, n] complex64 CUDA tensor (fb_fft1d_batched)."""
+    _fft_check(x)
+    out = torch.empty_like(x) if out is None else out
+    _fft_check(out)
+    b, n = x.shape
+    f = lib().fb_ifft1d_batched if inverse else lib().fb_fft1d_batched
+    _check("fb_fft1d_batched", f(_ptr(x), _ptr(out), n, b, _stream(stream)))
     return out
 
 

@@ -203,6 +203,56 @@ fb_status fb_ifft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, si
     return fft_entry(x, y, n0, n1, ws, ws_bytes, stream, true);
 }
 
+static fb_status fft1d_entry(const void* x, void* y, int64_t n, int64_t batch, void* stream, bool inverse) {
+    clear_error();
+    if (batch < 1 || n < 1) {
+        set_error("n and batch must be >= 1");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!is_pow2(n) || n > kTwN) {
+        set_error("line length must be a power of two in [1, %d] (got %lld)", kTwN, (long long)n);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
+    if (!x || !y) {
+        set_error("null x or y");
+        return FB_ERR_INVALID_VALUE;
+    }
+    if (!aligned16(x) || !aligned16(y)) {
+        set_error("x and y must be 16-byte aligned");
+        return FB_ERR_MISALIGNED;
+    }
+    const size_t bytes = (size_t)n * (size_t)batch * sizeof(float2);
+    if (ranges_partially_overlap(x, bytes, y, bytes)) {
+        set_error("x and y partially overlap (exact aliasing is allowed)");
+        return FB_ERR_INVALID_VALUE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    FftPass p{};
+    p.in = (const float2*)x;
+    p.out = (float2*)y;
+    p.log2L = ilog2(n);
+    p.nlines = batch;
+    p.g_shift = 0;
+    p.lin.hi = p.lout.hi = n;
+    p.lin.lo = p.lout.lo = 0;
+    p.lin.kb_shift = p.lout.kb_shift = 30;
+    p.lin.es = p.lout.es = 1;
+    p.lin.bs = p.lout.bs = 0;
+    p.conj_in = inverse;
+    p.conj_out = inverse;
+    p.scale = inverse ? 1.0f / (float)n : 1.0f;
+    return launch_fft_pass(p, st, (cudaStream_t)stream);
+}
+
+fb_status fb_fft1d_batched(const void* x, void* y, int64_t n, int64_t batch, void* stream) {
+    return fft1d_entry(x, y, n, batch, stream, false);
+}
+
+fb_status fb_ifft1d_batched(const void* x, void* y, int64_t n, int64_t batch, void* stream) {
+    return fft1d_entry(x, y, n, batch, stream, true);
+}
+
 size_t fb_matmul_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
     if ((dtype != FB_F32 && dtype != FB_F64) || m <= 0 || n <= 0 || k <= 0) return 0;
     return gemm_ws_bytes(dtype, m, n, k);

@@ -97,3 +97,13 @@ def test_slab_model_and_fused_query_validation(L):
     assert L.fb_fft2d_slab_model(9, 0, p, p, 64, 64, p, p, 1 << 20, None) == 1   # P > 8
     assert L.fb_fft2d_slab_model(4, 0, p, p, 64, 2, p, p, 1 << 20, None) == 2    # n1 % P
     assert L.fb_fft2d_slab_model(2, 0, p, p, 64, 64, p, p, 16, None) == 4        # workspace
+
+
+def test_fft1d_batched_validation(L):
+    p = ctypes.c_void_p(1 << 20)
+    assert L.fb_fft1d_batched(p, p, 3, 4, None) == 2        # not a power of two
+    assert L.fb_fft1d_batched(p, p, 32768, 4, None) == 2    # > 16384
+    assert L.fb_fft1d_batched(p, p, 16, 0, None) == 1       # empty batch
+    assert L.fb_ifft1d_batched(None, p, 16, 2, None) == 1
+    assert L.fb_fft1d_batched(ctypes.c_void_p(8), p, 16, 2, None) == 3
+    assert L.fb_fft1d_batched(p, ctypes.c_void_p((1 << 20) + 64), 16, 2, None) == 1  # partial overlap

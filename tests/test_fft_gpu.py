@@ -215,3 +215,31 @@ def test_pair_plan_matches_plain_plan(fb, n0, n1, monkeypatch):
     assert oracle.rel_l2(y_pair.cpu().numpy(), y_plain.cpu().numpy()) < 5e-7
     assert oracle.rel_l2(z_pair.cpu().numpy(), x.cpu().numpy()) < 5e-7
     assert oracle.rel_l2(z_plain.cpu().numpy(), x.cpu().numpy()) < 5e-7
+
+
+@pytest.mark.parametrize("n,batch", [(1, 3), (2, 5), (16, 7), (64, 33), (512, 40), (2048, 9), (4096, 4),
+                                     (8192, 3), (16384, 2)])
+def test_fft1d_batched_vs_oracle(fb, n, batch):
+    """fb_fft1d_batched / fb_ifft1d_batched against the 1D DFT definition."""
+    xh = synth.complex_field(batch, n)
+    x = torch.from_numpy(xh).cuda()
+    y = fb.fft1d(x)
+    z = fb.fft1d(y, inverse=True)
+    w = x.clone()
+    fb.fft1d(w, out=w)  # in place
+    torch.cuda.synchronize()
+    bar = 5e-7 if n <= 4096 else 1e-6
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.dft1d_rows(xh)) < bar
+    assert oracle.rel_l2(z.cpu().numpy(), xh) < bar
+    assert torch.equal(w, y)
+
+
+def test_fft1d_batched_matches_fft2d_rows(fb):
+    """A batch of lines is the row pass of the 2D transform with n0 = 1 per line."""
+    xh = synth.complex_field(8, 1024)
+    x = torch.from_numpy(xh).cuda()
+    y = fb.fft1d(x)
+    for b in (0, 7):
+        yb = fb.fft2d(x[b:b + 1].contiguous())
+        torch.cuda.synchronize()
+        assert oracle.rel_l2(y[b:b + 1].cpu().numpy(), yb.cpu().numpy()) < 1e-6

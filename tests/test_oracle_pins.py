@@ -235,3 +235,34 @@ def test_synth_recipe():
     assert np.array_equal(v, np.round(v))
     bits = a.view(np.uint32) & 0x1FFF
     assert np.mean(bits != 0) > 0.9
+
+
+# ---------------------------------------------------------------- batched 1D DFT (N4)
+def test_dft1d_rows_hand_and_closed_forms():
+    """n = 2 by hand ([a, b] -> [a + b, a - b]); delta at t0 -> exp(-2 pi i k t0 / n); a
+    single tone exp(+2 pi i f t / n) -> n at k = f; inverse o forward = identity."""
+    x = np.array([[1 + 2j, 3 - 1j], [0.5, -0.25j]], dtype=np.complex64)
+    X = oracle.dft1d_rows(x)
+    assert np.allclose(X, [[4 + 1j, -2 + 3j], [0.5 - 0.25j, 0.5 + 0.25j]], atol=1e-15)
+    n = 64
+    k = np.arange(n)
+    d = np.zeros((3, n), dtype=np.complex64)
+    for b, t0 in enumerate((0, 5, 63)):
+        d[b, t0] = 1
+    D = oracle.dft1d_rows(d)
+    for b, t0 in enumerate((0, 5, 63)):
+        assert np.allclose(D[b], np.exp(-2j * np.pi * k * t0 / n), atol=1e-14)
+    f = 7
+    tone = np.exp(2j * np.pi * f * k / n)[None, :]
+    T = oracle.dft1d_rows(tone)
+    ref = np.zeros(n, dtype=complex)
+    ref[f] = n
+    assert np.abs(T[0] - ref).max() < 1e-12
+    x = synth.complex_field(5, 32)
+    assert oracle.rel_l2(oracle.dft1d_rows(oracle.dft1d_rows(x), inverse=True), x) < 1e-14
+
+
+def test_dft1d_rows_vs_numpy():
+    x = synth.complex_field(9, 128)
+    assert oracle.rel_l2(oracle.dft1d_rows(x), np.fft.fft(x.astype(np.complex128), axis=1)) < 1e-14
+    assert oracle.rel_l2(oracle.dft1d_rows(x, inverse=True), np.fft.ifft(x.astype(np.complex128), axis=1)) < 1e-14
