@@ -106,6 +106,18 @@ fb_status fb_ifft1d_batched(const void* x, void* y, int64_t n, int64_t batch, vo
  * ws: device workspace of fb_matmul_workspace_bytes(...) bytes (FP32: the TF32 hi/lo
  * split operands; FP64: 0).  C must not overlap A, B or ws. */
 size_t fb_matmul_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k);
+
+/* BLAS-style variant: C = alpha op(A) op(B) + beta C, op(X) = X (trans 0) or
+ * X^T (trans 1); op(A) is m x k (A stored m x k, lda >= k; or k x m, lda >= m), op(B) is k x n
+ * (B stored k x n, ldb >= n; or n x k, ldb >= k).  Same arithmetic and accuracy as fb_matmul
+ * (the product is formed by the same kernels, then alpha, beta are applied in FP32 / FP64).
+ * beta == 0: C is not read (NaN in C does not propagate); alpha == 0: A and B are not read.
+ * Alignment rules as fb_matmul.  ws: fb_gemm_workspace_bytes(...) bytes (transposed operand
+ * copies + the fb_matmul workspace + an m x n product tile). */
+size_t fb_gemm_workspace_bytes(int dtype, int transA, int transB, int64_t m, int64_t n, int64_t k);
+fb_status fb_gemm(int dtype, int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,
+                  const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,
+                  int64_t ldc, void* ws, size_t ws_bytes, void* stream);
 fb_status fb_matmul(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                     const void* B, int64_t ldb, void* C, int64_t ldc, void* ws,
                     size_t ws_bytes, void* stream);

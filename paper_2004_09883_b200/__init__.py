@@ -28,6 +28,7 @@ _STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_VALUE", 2: "FB_ERR_UNSUPPORTED_SIZE", 
 EXPORTS = [
     "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_init",
     "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d", "fb_fft1d_batched", "fb_ifft1d_batched",
+    "fb_gemm_workspace_bytes", "fb_gemm",
     "fb_matmul_workspace_bytes", "fb_matmul", "fb_tf32_split", "fb_matmul_3xtf32_presplit",
     "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
@@ -68,6 +69,9 @@ def lib() -> ctypes.CDLL:
         "fb_fft1d_batched": ([vp, vp, i64, i64, vp], ci),
         "fb_ifft1d_batched": ([vp, vp, i64, i64, vp], ci),
         "fb_matmul_workspace_bytes": ([ci, i64, i64, i64], sz),
+        "fb_gemm_workspace_bytes": ([ci, ci, ci, i64, i64, i64], sz),
+        "fb_gemm": ([ci, ci, ci, i64, i64, i64, ctypes.c_double, vp, i64, vp, i64, ctypes.c_double, vp, i64, vp,
+                     sz, vp], ci),
         "fb_matmul": ([ci, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], ci),
         "fb_tf32_split": ([ci, i64, i64, vp, i64, vp, vp, i64, vp], ci),
         "fb_matmul_3xtf32_presplit": ([i64, i64, i64, vp, vp, i64, vp, vp, i64, vp, i64, vp], ci),
@@ -185,6 +189,22 @@ def ifft2d(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> tor
 
 
 # ------------------------------------------------------------------ matrix block
+def gemm(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, alpha: float = 1.0, beta: float = 0.0,
+         trans_a: bool = False, trans_b: bool = False, stream=None) -> torch.Tensor:
+    """C = alpha op(A) op(B) + beta C (fb_gemm); float32 (3xTF32) or float64 (DMMA)."""
+    dt = _dt(A)
+    m = A.shape[1] if trans_a else A.shape[0]
+    k = A.shape[0] if trans_a else A.shape[1]
+    n = B.shape[0] if trans_b else B.shape[1]
+    if C is None:
+        C = torch.zeros(m, n, dtype=A.dtype, device=A.device)
+    ws = _workspace_named(lib().fb_gemm_workspace_bytes(dt, int(trans_a), int(trans_b), m, n, k), A.device, "gemm")
+    _check("fb_gemm", lib().fb_gemm(dt, int(trans_a), int(trans_b), m, n, k, float(alpha), _ptr(A), A.stride(0),
+                                    _ptr(B), B.stride(0), float(beta), _ptr(C), C.stride(0), _ptr(ws), ws.numel(),
+                                    _stream(stream)))
+    return C
+
+
 def _dt(t: torch.Tensor) -> int:
     if t.dtype == torch.float32:
         return FB_F32

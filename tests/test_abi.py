@@ -107,3 +107,15 @@ def test_fft1d_batched_validation(L):
     assert L.fb_ifft1d_batched(None, p, 16, 2, None) == 1
     assert L.fb_fft1d_batched(ctypes.c_void_p(8), p, 16, 2, None) == 3
     assert L.fb_fft1d_batched(p, ctypes.c_void_p((1 << 20) + 64), 16, 2, None) == 1  # partial overlap
+
+
+def test_gemm_ex_validation(L):
+    p = ctypes.c_void_p(1 << 20)
+    ws = ctypes.c_void_p(1 << 30)
+    big = 1 << 40
+    assert L.fb_gemm(2, 0, 0, 4, 4, 4, 1.0, p, 4, p, 4, 0.0, p, 4, ws, big, None) == 1   # dtype
+    assert L.fb_gemm(1, 2, 0, 4, 4, 4, 1.0, p, 4, p, 4, 0.0, p, 4, ws, big, None) == 1   # trans flag
+    assert L.fb_gemm(1, 1, 0, 8, 4, 4, 1.0, p, 4, p, 4, 0.0, ctypes.c_void_p(1 << 24), 4, ws, big, None) == 1  # lda < m
+    assert L.fb_gemm(1, 0, 0, 4, 4, 4, 1.0, p, 4, ctypes.c_void_p(1 << 22), 4, 0.0,
+                     ctypes.c_void_p(1 << 24), 4, None, 0, None) == 4                       # workspace
+    assert L.fb_gemm_workspace_bytes(1, 1, 1, 64, 64, 64) > L.fb_gemm_workspace_bytes(1, 0, 0, 64, 64, 64)

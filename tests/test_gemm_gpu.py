@@ -144,3 +144,41 @@ def test_host_variant(fb):
     C = torch.empty(m, n).pin_memory()
     fb.fb_matmul_host(A, B, C)
     assert oracle.rel_l2(C.numpy(), oracle.matmul(A.numpy(), B.numpy())) < 1e-5
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("ta,tb", [(0, 0), (1, 0), (0, 1), (1, 1)])
+def test_gemm_ex_transposes_alpha_beta(fb, dt, ta, tb):
+    """fb_gemm: C = alpha op(A) op(B) + beta C against the oracle product of the
+    explicitly transposed operands, combined with alpha, beta in FP64."""
+    m, n, k = 200, 136, 72
+    Ah = synth.real_matrix(k if ta else m, m if ta else k, synth.TID_GEMM_A)
+    Bh = synth.real_matrix(n if tb else k, k if tb else n, synth.TID_GEMM_B)
+    C0 = synth.real_matrix(m, n, synth.TID_NOISE)
+    opA = Ah.T if ta else Ah
+    opB = Bh.T if tb else Bh
+    P = oracle.matmul(np.ascontiguousarray(opA).astype(np.float64), np.ascontiguousarray(opB).astype(np.float64))
+    bar = 1e-5 if dt == torch.float32 else 1e-12
+    for alpha, beta in [(1.0, 0.0), (0.75, -0.5), (-2.0, 1.0)]:
+        A = torch.from_numpy(np.ascontiguousarray(Ah)).to(dt).cuda()
+        B = torch.from_numpy(np.ascontiguousarray(Bh)).to(dt).cuda()
+        C = torch.from_numpy(C0).to(dt).cuda()
+        fb.gemm(A, B, C, alpha, beta, bool(ta), bool(tb))
+        torch.cuda.synchronize()
+        ref = alpha * P + beta * C0.astype(np.float64)
+        assert oracle.rel_l2(C.cpu().numpy(), ref) < bar, (alpha, beta)
+
+
+def test_gemm_ex_beta0_ignores_nan_and_alpha0(fb):
+    m, n, k = 64, 48, 40
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).double().cuda()
+    B = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).double().cuda()
+    C = torch.full((m, n), float("nan"), dtype=torch.float64, device="cuda")
+    fb.gemm(A, B, C, 1.5, 0.0)
+    ref = 1.5 * oracle.matmul(A.cpu().numpy(), B.cpu().numpy())
+    torch.cuda.synchronize()
+    assert torch.isfinite(C).all() and oracle.rel_l2(C.cpu().numpy(), ref) < 1e-12
+    C2 = torch.ones(m, n, dtype=torch.float64, device="cuda")
+    fb.gemm(A, B, C2, 0.0, 3.0)
+    torch.cuda.synchronize()
+    assert torch.equal(C2, torch.full_like(C2, 3.0))
