@@ -95,6 +95,17 @@ fb_status fb_ifft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, si
 fb_status fb_fft1d_batched(const void* x, void* y, int64_t n, int64_t batch, void* stream);
 fb_status fb_ifft1d_batched(const void* x, void* y, int64_t n, int64_t batch, void* stream);
 
+/* Real-input 2D transform (the paper's vibration signals are real):
+ * x is an n0 x n1 row-major float32 array, y the Hermitian half of its DFT, an n0 x (n1/2+1)
+ * row-major complex64 array (numpy rfft2 / cuFFT R2C layout):
+ *   y[k0][k1] = sum_{t0,t1} x[t0][t1] exp(-2 pi i (k0 t0/n0 + k1 t1/n1)), 0 <= k1 <= n1/2.
+ * fb_irfft2d is the exact inverse (sign +1, 1/(n0 n1); y read, never written).  n0, n1 powers
+ * of two, 1 <= n0 <= 16384, 2 <= n1 <= 16384.  x, y, ws 16-byte aligned and pairwise
+ * disjoint; ws: fb_rfft2d_workspace_bytes(n0, n1) bytes.  Accuracy as fb_fft2d. */
+size_t fb_rfft2d_workspace_bytes(int64_t n0, int64_t n1);
+fb_status fb_rfft2d(const void* x, void* y, int64_t n0, int64_t n1, void* ws, size_t ws_bytes, void* stream);
+fb_status fb_irfft2d(const void* y, void* x, int64_t n0, int64_t n1, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------ matrix block
  * C[m][n] = A[m][k] * B[k][n]  (row-major, leading dimensions in ELEMENTS, C overwritten).
  * FB_F64: IEEE FP64 (DMMA tensor-core FMAs, RN); accuracy rel-L2 <= 1e-12.

@@ -28,7 +28,7 @@ _STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_VALUE", 2: "FB_ERR_UNSUPPORTED_SIZE", 
 EXPORTS = [
     "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_init",
     "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d", "fb_fft1d_batched", "fb_ifft1d_batched",
-    "fb_gemm_workspace_bytes", "fb_gemm",
+    "fb_gemm_workspace_bytes", "fb_gemm", "fb_rfft2d_workspace_bytes", "fb_rfft2d", "fb_irfft2d",
     "fb_matmul_workspace_bytes", "fb_matmul", "fb_tf32_split", "fb_matmul_3xtf32_presplit",
     "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
@@ -67,6 +67,9 @@ def lib() -> ctypes.CDLL:
         "fb_fft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
         "fb_ifft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
         "fb_fft1d_batched": ([vp, vp, i64, i64, vp], ci),
+        "fb_rfft2d_workspace_bytes": ([i64, i64], sz),
+        "fb_rfft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
+        "fb_irfft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
         "fb_ifft1d_batched": ([vp, vp, i64, i64, vp], ci),
         "fb_matmul_workspace_bytes": ([ci, i64, i64, i64], sz),
         "fb_gemm_workspace_bytes": ([ci, ci, ci, i64, i64, i64], sz),
@@ -182,6 +185,28 @@ def fft1d(x: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = Fals
     f = lib().fb_ifft1d_batched if inverse else lib().fb_fft1d_batched
     _check("fb_fft1d_batched", f(_ptr(x), _ptr(out), n, b, _stream(stream)))
     return out
+
+
+def rfft2d(x: torch.Tensor, stream=None) -> torch.Tensor:
+    """Hermitian half [n0, n1/2+1] (complex64) of the 2D DFT of a real float32 CUDA tensor."""
+    if x.dtype != torch.float32 or not x.is_cuda or x.dim() != 2 or not x.is_contiguous():
+        raise ValueError("expected a contiguous 2D float32 CUDA tensor")
+    n0, n1 = x.shape
+    y = torch.empty(n0, n1 // 2 + 1, dtype=torch.complex64, device=x.device)
+    ws = _workspace_named(lib().fb_rfft2d_workspace_bytes(n0, n1), x.device, "rfft")
+    _check("fb_rfft2d", lib().fb_rfft2d(_ptr(x), _ptr(y), n0, n1, _ptr(ws), ws.numel(), _stream(stream)))
+    return y
+
+
+def irfft2d(y: torch.Tensor, n1: int, stream=None) -> torch.Tensor:
+    """Real [n0, n1] inverse of rfft2d (scaled 1/(n0 n1))."""
+    if y.dtype != torch.complex64 or not y.is_cuda or y.dim() != 2 or not y.is_contiguous():
+        raise ValueError("expected a contiguous 2D complex64 CUDA tensor")
+    n0 = y.shape[0]
+    x = torch.empty(n0, n1, dtype=torch.float32, device=y.device)
+    ws = _workspace_named(lib().fb_rfft2d_workspace_bytes(n0, n1), y.device, "rfft")
+    _check("fb_irfft2d", lib().fb_irfft2d(_ptr(y), _ptr(x), n0, n1, _ptr(ws), ws.numel(), _stream(stream)))
+    return x
 
 
 def ifft2d(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:

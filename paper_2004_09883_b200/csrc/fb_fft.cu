@@ -82,6 +82,18 @@ fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, 
         p.col_like = 1;
         return launch_fft_pass(p, st, s);
     }
+    // the four-step line numbering (g = n2 * ncols + c) needs a power-of-two column count:
+    // other counts run as power-of-two column blocks
+    if (!is_pow2(ncols)) {
+        int64_t c0 = 0;
+        for (int bit = 62; bit >= 0; --bit) {
+            const int64_t w = int64_t(1) << bit;
+            if (!(ncols & w)) continue;
+            FB_TRY(fft_columns(in + c0, out + c0, n0, w, ld_in, ld_out, conj_in, conj_out, scale, tmp, st, s));
+            c0 += w;
+        }
+        return FB_OK;
+    }
     // Four-step split of the column length n0 = a * b (b = 128 contiguous sub-line rows):
     //   step 1: for each n2 < b: length-a FFTs over rows b*n1 + n2, times W_n0^{n2 k1}
     //           (tmp rows b*k1 + n2)

@@ -119,3 +119,14 @@ def test_gemm_ex_validation(L):
     assert L.fb_gemm(1, 0, 0, 4, 4, 4, 1.0, p, 4, ctypes.c_void_p(1 << 22), 4, 0.0,
                      ctypes.c_void_p(1 << 24), 4, None, 0, None) == 4                       # workspace
     assert L.fb_gemm_workspace_bytes(1, 1, 1, 64, 64, 64) > L.fb_gemm_workspace_bytes(1, 0, 0, 64, 64, 64)
+
+
+def test_rfft2d_validation(L):
+    p = ctypes.c_void_p(1 << 20)
+    q = ctypes.c_void_p(1 << 24)
+    w = ctypes.c_void_p(1 << 28)
+    assert L.fb_rfft2d(p, q, 4, 1, w, 1 << 20, None) == 1        # n1 < 2
+    assert L.fb_rfft2d(p, q, 3, 8, w, 1 << 20, None) == 2        # not a power of two
+    assert L.fb_rfft2d(p, q, 4, 8, None, 0, None) == 4           # workspace
+    assert L.fb_irfft2d(p, ctypes.c_void_p((1 << 20) + 16), 4, 8, w, 1 << 20, None) == 1  # overlap
+    assert L.fb_rfft2d_workspace_bytes(64, 64) >= 64 * 32 * 8 + 64 * 33 * 8

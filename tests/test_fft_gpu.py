@@ -243,3 +243,42 @@ def test_fft1d_batched_matches_fft2d_rows(fb):
         yb = fb.fft2d(x[b:b + 1].contiguous())
         torch.cuda.synchronize()
         assert oracle.rel_l2(y[b:b + 1].cpu().numpy(), yb.cpu().numpy()) < 1e-6
+
+
+def _real_field(n0, n1):
+    return np.ascontiguousarray(synth.complex_field(n0, n1 // 2).view(np.float32).reshape(n0, n1))
+
+
+@pytest.mark.parametrize("n0,n1", [(1, 2), (2, 2), (4, 8), (64, 128), (256, 256), (512, 64), (2048, 2048),
+                                   (8192, 64), (16, 16384)])
+def test_rfft2d_vs_oracle(fb, n0, n1):
+    """fb_rfft2d / fb_irfft2d (real vibration signals P:149): the Hermitian half of
+    the 2D DFT definition of the real input, and the exact inverse."""
+    xr = _real_field(n0, n1)
+    x = torch.from_numpy(xr).cuda()
+    y = fb.rfft2d(x)
+    z = fb.irfft2d(y, n1)
+    torch.cuda.synchronize()
+    h = n1 // 2
+    if n0 * n1 <= 2048 * 2048:
+        ref = oracle.dft2d(xr.astype(np.complex64))[:, :h + 1]
+    else:  # sampled full columns of the oracle
+        cols = [0, 1, h // 2, h]
+        ref = np.stack([oracle.dft2d_col(xr.astype(np.complex64), c) for c in cols], axis=1)
+        y = y[:, cols]
+    bar = max(5e-7, 1e-7 * np.log2(n0 * n1))
+    assert oracle.rel_l2(y.cpu().numpy(), ref) < bar
+    assert oracle.rel_l2(z.cpu().numpy(), xr) < bar
+
+
+def test_irfft2d_vs_oracle_inverse(fb):
+    """The inverse of a Hermitian half equals the oracle's inverse DFT of the Hermitian
+    extension (real part; the imaginary part of the oracle result is ~0)."""
+    n0, n1 = 64, 32
+    X = oracle.dft2d(_real_field(n0, n1).astype(np.complex64))
+    half = np.ascontiguousarray(X[:, :n1 // 2 + 1].astype(np.complex64))
+    z = fb.irfft2d(torch.from_numpy(half).cuda(), n1)
+    torch.cuda.synchronize()
+    ref = oracle.dft2d(X.astype(np.complex64), inverse=True)
+    assert np.abs(ref.imag).max() < 1e-5
+    assert oracle.rel_l2(z.cpu().numpy(), ref.real) < 5e-7
