@@ -854,16 +854,24 @@ static fb_status lu_tensor_map(CUtensorMap* m, double* A, int64_t n, int64_t lda
 }
 
 template <int PT, int RPT, int PNB>
+static fb_status lu_la_attrs() {  // outside any stream capture
+    static bool attr = false;
+    if (!attr) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_la_kernel<PT, RPT, PNB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_tma_kernel<PT, RPT, PNB>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+        attr = true;
+    }
+    return FB_OK;
+}
+
+template <int PT, int RPT, int PNB>
 static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
     constexpr int nb = PNB;
     auto panel = lu::lu_panel_la_kernel<PT, RPT, PNB>;
     auto panel_tma = lu::lu_panel_tma_kernel<PT, RPT, PNB>;
-    static bool attr = false;
-    if (!attr) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(panel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        FB_CUDA_TRY(cudaFuncSetAttribute(panel_tma, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
-    }
+    FB_TRY((lu_la_attrs<PT, RPT, PNB>()));
     const char* tk = getenv("FB_LU_TMA");  // A/B knob: 0 = cp.async panel kernel
     const bool use_tma = !(tk && tk[0] == '0') && (lda * 8) % 16 == 0 && ((uintptr_t)A & 15) == 0;
     CUtensorMap tmA;
@@ -929,11 +937,78 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
     return FB_OK;
 }
 
+// The look-ahead schedule (~3 n/8 kernels + events on two streams) is captured once per
+// (A, n, lda, ipiv, info, device) into a CUDA graph and replayed on the caller's stream: the
+// per-step dependency resolution happens inside the graph instead of through stream/event
+// round trips (knob FB_LU_GRAPH=0 enqueues the schedule directly).  A small per-thread cache
+// holds the instantiated graphs.
+struct LuGraph {
+    double* A = nullptr;
+    int64_t n = 0, lda = 0;
+    int32_t* ipiv = nullptr;
+    int32_t* info = nullptr;
+    int dev = -1;
+    cudaGraphExec_t exec = nullptr;
+};
+
+static fb_status lu_device_la_any(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
+    if (n <= 2048) return lu_device_la<512, 4, lu::NB>(n, A, lda, ipiv, info, s);
+    return lu_device_la<1024, 4, lu::NB / 2>(n, A, lda, ipiv, info, s);
+}
+
+static fb_status lu_device_graph(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
+    thread_local static LuGraph cache[4];
+    thread_local static int victim = 0;
+    thread_local static cudaStream_t cap[32] = {};
+    int dev = 0;
+    FB_CUDA_TRY(cudaGetDevice(&dev));
+    for (auto& g : cache)
+        if (g.exec && g.A == A && g.n == n && g.lda == lda && g.ipiv == ipiv && g.info == info && g.dev == dev) {
+            FB_CUDA_TRY(cudaGraphLaunch(g.exec, s));
+            return FB_OK;
+        }
+    FB_TRY((n <= 2048 ? lu_la_attrs<512, 4, lu::NB>() : lu_la_attrs<1024, 4, lu::NB / 2>()));
+    if (!cap[dev & 31]) FB_CUDA_TRY(cudaStreamCreateWithFlags(&cap[dev & 31], cudaStreamNonBlocking));
+    cudaStream_t cs = cap[dev & 31];
+    FB_CUDA_TRY(cudaStreamBeginCapture(cs, cudaStreamCaptureModeThreadLocal));
+    const fb_status st = lu_device_la_any(n, A, lda, ipiv, info, cs);
+    cudaGraph_t graph = nullptr;
+    const cudaError_t ce = cudaStreamEndCapture(cs, &graph);
+    if (st != FB_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+    }
+    if (ce != cudaSuccess) {
+        set_error("LU graph capture failed: %s", cudaGetErrorString(ce));
+        return FB_ERR_CUDA;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ie != cudaSuccess) {
+        set_error("LU graph instantiation failed: %s", cudaGetErrorString(ie));
+        return FB_ERR_CUDA;
+    }
+    LuGraph& g = cache[victim];
+    victim = (victim + 1) % 4;
+    if (g.exec) cudaGraphExecDestroy(g.exec);
+    g.A = A;
+    g.n = n;
+    g.lda = lda;
+    g.ipiv = ipiv;
+    g.info = info;
+    g.dev = dev;
+    g.exec = exec;
+    FB_CUDA_TRY(cudaGraphLaunch(exec, s));
+    return FB_OK;
+}
+
 fb_status lu_device(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
     const char* la = getenv("FB_LU_LOOKAHEAD");
     if (!(la && la[0] == '0')) {
-        if (n <= 2048) return lu_device_la<512, 4, lu::NB>(n, A, lda, ipiv, info, s);
-        return lu_device_la<1024, 4, lu::NB / 2>(n, A, lda, ipiv, info, s);
+        const char* gk = getenv("FB_LU_GRAPH");
+        if (!(gk && gk[0] == '0')) return lu_device_graph(n, A, lda, ipiv, info, s);
+        return lu_device_la_any(n, A, lda, ipiv, info, s);
     }
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     const bool small = n <= 2048;
