@@ -10,4 +10,6 @@ timeout 600 $HCMD > /dev/null 2>&1 || exit 1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fft_pass" -s 10 -c 2 -o gpurun_out/${R}_fft2048 $HCMD > gpurun_out/${R}_fft2048.log 2>&1
 GCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --only gemm_f32_2048,gemm_f64_2048,lu_f64_2048"
 timeout 600 $GCMD > /dev/null 2>&1 || exit 1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:"gemm_3xtf32|gemm_f64_dmma|split_|lu_panel_la|lu_rank|lu_swap" -s 3 -c 10 -o gpurun_out/${R}_gemm_lu $GCMD > gpurun_out/${R}_gemm_lu.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_3xtf32|split_both" -s 2 -c 2 -o gpurun_out/${R}_gemm $GCMD > gpurun_out/${R}_gemm.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_f64_dmma" -s 1 -c 1 -o gpurun_out/${R}_f64 $GCMD > gpurun_out/${R}_f64.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"lu_panel_tma|lu_rank|lu_swap" -s 60 -c 3 -o gpurun_out/${R}_lu $GCMD > gpurun_out/${R}_lu.log 2>&1
