@@ -184,6 +184,18 @@ static fb_status ensure_window(fb_comm* c, size_t bytes) {
     return FB_OK;
 }
 
+// A window that cannot be allocated or registered (e.g. no symmetric-memory support for this
+// size) turns the communicator's fused path off for good; the call proceeds on ncclAlltoAll.
+static fb_status ensure_window_or_fallback(fb_comm* c, size_t bytes) {
+    const fb_status st = ensure_window(c, bytes);
+    if (st != FB_OK) {
+        snprintf(c->fused_why, sizeof(c->fused_why), "symmetric window of %zu bytes unavailable: %s", bytes,
+                 fb_last_error_detail());
+        clear_error();
+    }
+    return st;
+}
+
 // The fused passes, shared by the real path and the single-GPU model (fb_fft2d_slab_model).
 // win[d] = base of rank d's receive window (n0 x cols natural column strip).
 // Forward row pass of rank r: row i of the slab -> element k to win[k / cols][(r rows + i) cols + k mod cols].
@@ -324,8 +336,8 @@ fb_status fb_fft2d_slab(fb_comm* c, const void* x_rows, void* y_cols, int64_t n0
     const size_t slab = (size_t)rows * n1;
     float2* send = (float2*)ws;
     float2* recv = send + slab;
+    if (c->fused && ensure_window_or_fallback(c, slab * sizeof(float2)) != FB_OK) c->fused = 0;
     if (c->fused) {
-        FB_TRY(ensure_window(c, slab * sizeof(float2)));
         FB_TRY(lsa_barrier(c, s));  // every peer is done with its window (previous call)
         FB_TRY(slab_rows_push((const float2*)x_rows, c->peer_base, c->rank, P, n0, n1, st, s));
         FB_TRY(lsa_barrier(c, s));  // every peer's blocks have landed in this rank's window
@@ -361,8 +373,8 @@ fb_status fb_ifft2d_slab(fb_comm* c, const void* y_cols, void* x_rows, int64_t n
     const size_t slab = (size_t)rows * n1;
     float2* send = (float2*)ws;
     float2* recv = send + slab;
+    if (c->fused && ensure_window_or_fallback(c, slab * sizeof(float2)) != FB_OK) c->fused = 0;
     if (c->fused) {
-        FB_TRY(ensure_window(c, slab * sizeof(float2)));
         FB_TRY(lsa_barrier(c, s));  // no peer still reads this rank's window (previous call)
         FB_TRY(fft_columns((const float2*)y_cols, (float2*)c->win_buf, n0, cols, cols, cols, true, false, 1.f, send,
                            st, s));
