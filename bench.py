@@ -432,7 +432,40 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                                            "frac": ach / pk["hbm_gbs"],
                                            "note": f"{passes} HBM passes x (R+W) of the 2 GiB array"}}
         del x, y, ws
+    if want("gemm_f32_32768"):  # configs[4] at 1 GPU: the scaling baseline of the row-block GEMM
+        res["gemm_f32_32768"] = rowblock_gemm(args, torch, fb, np, stream, flush, pk, None, 0, 1, None)
     return res
+
+
+def rowblock_gemm(args, torch, fb, np, stream, flush, pk, dist, rank, world, comm):
+    """configs[4]: C = A B, 32768^3 FP32 (3xTF32), A and C row-sharded over `world` ranks, B broadcast
+    from rank 0 inside the timed region (fb_matmul_rowblock; plain fb_matmul at world size 1)."""
+    n = 32768
+    rows = n // world
+    g = torch.Generator(device="cuda").manual_seed(200409883 + rank)
+    A = (torch.rand(rows, n, device="cuda", generator=g) * 2 - 1)
+    B = (torch.rand(n, n, device="cuda", generator=torch.Generator(device="cuda").manual_seed(200409884)) * 2 - 1)
+    C = torch.empty(rows, n, device="cuda")
+    if comm is None:
+        ws = torch.empty(fb.matmul_workspace_bytes(fb.FB_F32, rows, n, n), dtype=torch.uint8, device="cuda")
+        fn = lambda: fb.fb_matmul(A, B, C, ws, stream)  # noqa: E731
+    else:
+        ws = torch.empty(fb.lib().fb_matmul_rowblock_workspace_bytes(world, fb.FB_F32, n, n, n), dtype=torch.uint8,
+                         device="cuda")
+        fn = lambda: comm.fb_matmul_rowblock(A, B, C, root=0, ws=ws, stream=stream)  # noqa: E731
+    ms = timed_steps(torch, fn, 3, min(args.warmup, 3), flush, stream, dist)
+    t = max_over_ranks(torch, dist, float(np.mean(ms)))
+    del A, B, C, ws
+    flops = 2.0 * n * n * n
+    tf32_peak = pk["bf16_tflops_sustained"] / 2.0
+    return {"value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
+            "config": {"workload": "gemm_32768^3_fp32_3xtf32_rowblock", "configs_index": 4,
+                       "parallelism": f"rowblock{world}", "data": "uniform [-1, 1) (torch, seeded, on device)",
+                       "b_broadcast": "ncclBroadcast inside the timed region" if comm is not None else "none"},
+            "roofline": {"bound": "tensor", "achieved": 3 * flops / world / (t * 1e-3) / 1e12, "peak": tf32_peak,
+                         "unit": "TFLOP/s", "frac": 3 * flops / world / (t * 1e-3) / 1e12 / tf32_peak,
+                         "note": "per GPU, counting the 3 TF32 MMAs (6MNK/P), split pre-pass and broadcast "
+                                 "inside the time; peak = sustained BF16 x 0.5"}}
 
 
 def run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, local):
@@ -463,6 +496,8 @@ def run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, l
     me = timed_steps(torch, e2e_step, max(2, args.steps // 2), args.warmup, flush, stream, dist)
     te = max_over_ranks(torch, dist, float(np.mean(me)))
     fused = comm.fused
+    del xh, yh, x, y, ws
+    gemm = rowblock_gemm(args, torch, fb, np, stream, flush, pk, dist, rank, world, comm)
     comm.destroy()
     val = fft_flops(n, n) / (t * 1e-3) / 1e9
     hbm = 3 * 2 * 8 * n * n / world  # 3 local passes (row, 2 four-step column passes), R+W
@@ -478,7 +513,8 @@ def run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, l
             "e2e": {"value": fft_flops(n, n) / (te * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": te,
                     "h2d_bytes_per_step": rows * n * 8, "d2h_bytes_per_step": n * (n // world) * 8,
                     "api": "pinned torch copies + fb_fft2d_slab, per rank"},
-            "gpu_launches": launches * args.steps, "clocks": clk.summary()}
+            "gpu_launches": launches * args.steps, "clocks": clk.summary(),
+            "blocks": {"gemm_f32_32768_rowblock": gemm}}
 
 
 if __name__ == "__main__":
