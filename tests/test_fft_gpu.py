@@ -282,3 +282,20 @@ def test_irfft2d_vs_oracle_inverse(fb):
     ref = oracle.dft2d(X.astype(np.complex64), inverse=True)
     assert np.abs(ref.imag).max() < 1e-5
     assert oracle.rel_l2(z.cpu().numpy(), ref.real) < 5e-7
+
+
+@pytest.mark.parametrize("knobs", [{"FB_FFT_NO_TMA": "1"}, {"FB_FFT_PAIR_TMA": "0"}, {"FB_FFT_ROW_NB": "2"},
+                                   {"FB_FFT_COL_NB": "2"}, {"FB_FFT_NO_PDL": "1"}, {"FB_FFT_COL_MAX_LOG2": "10"}])
+@pytest.mark.parametrize("n0,n1", [(512, 256), (2048, 128), (4096, 64)])
+def test_fft_path_variants_vs_oracle(fb, n0, n1, knobs, monkeypatch):
+    """Each kernel path behind an A/B knob (no TMA, plain-kernel pair row pass, forced staging
+    buffer counts, no PDL, four-step for shorter columns) computes the same DFT."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    xh = synth.complex_field(n0, n1)
+    x = torch.from_numpy(xh).cuda()
+    y = fb.fft2d(x)
+    z = fb.ifft2d(y)
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.dft2d(xh)) < 5e-7
+    assert oracle.rel_l2(z.cpu().numpy(), xh) < 5e-7

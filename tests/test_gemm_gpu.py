@@ -182,3 +182,19 @@ def test_gemm_ex_beta0_ignores_nan_and_alpha0(fb):
     fb.gemm(A, B, C2, 0.0, 3.0)
     torch.cuda.synchronize()
     assert torch.equal(C2, torch.full_like(C2, 3.0))
+
+
+@pytest.mark.parametrize("knobs,dt", [({"FB_GEMM_1CTA": "1"}, torch.float32), ({"FB_GEMM_SPLIT2": "1"}, torch.float32),
+                                      ({"FB_F64_CFG": "1"}, torch.float64), ({"FB_F64_CFG": "2"}, torch.float64)])
+def test_gemm_path_variants(fb, knobs, dt, monkeypatch):
+    """The kernels behind A/B knobs (1-CTA tcgen05 kernel, two split launches, the larger FP64
+    tile shapes) match the oracle like the defaults."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    m, n, k = 320, 264, 200
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(dt).cuda()
+    B = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).to(dt).cuda()
+    C = fb.matmul(A, B)
+    torch.cuda.synchronize()
+    bar = 1e-5 if dt == torch.float32 else 1e-12
+    assert oracle.rel_l2(C.cpu().numpy(), oracle.matmul(A.cpu().numpy(), B.cpu().numpy())) < bar

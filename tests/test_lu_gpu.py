@@ -97,3 +97,32 @@ def test_lu_repeated_outside_pivot_row(fb):
     A[0, 1] = 40.0    # ... which (after the rank-1 update) holds the step-1 pivot again
     A[30, 1] = 1.0
     _check(fb, np.ascontiguousarray(A))
+
+
+@pytest.mark.parametrize("knobs", [{"FB_LU_GRAPH": "0"}, {"FB_LU_TMA": "0"}, {"FB_LU_RANK_SIMT": "0"},
+                                   {"FB_LU_SERIAL": "1", "FB_LU_GRAPH": "0"}, {"FB_LU_LOOKAHEAD": "0"}])
+@pytest.mark.parametrize("n", [40, 777, 2048])
+def test_lu_schedule_variants(fb, n, knobs, monkeypatch):
+    """Every schedule / kernel variant behind an A/B knob (stream-ordered instead of graph,
+    cp.async instead of TMA panel, DMMA instead of streaming rank update, wide parts on one
+    stream, no look-ahead) gives the same pivots and factors within the oracle bar."""
+    for k, v in knobs.items():
+        monkeypatch.setenv(k, v)
+    _check(fb, synth.real_matrix(n, n, synth.TID_GEMM_A).astype(np.float64))
+
+
+def test_lu_graph_replay_reuses_buffers(fb):
+    """The cached graph replays on the same buffers with new contents (the key is the
+    pointers and sizes, not the data)."""
+    n = 1000
+    buf = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+    ipiv = torch.empty(n, dtype=torch.int32, device="cuda")
+    info = torch.zeros(1, dtype=torch.int32, device="cuda")
+    for seed_tid in (synth.TID_GEMM_A, synth.TID_GEMM_B, synth.TID_NOISE):
+        A = synth.real_matrix(n, n, seed_tid).astype(np.float64)
+        buf.copy_(torch.from_numpy(A))
+        fb.fb_lu(buf, ipiv, info)
+        torch.cuda.synchronize()
+        LU_o, ipiv_o, _ = oracle.lu(A)
+        assert np.array_equal(ipiv.cpu().numpy(), ipiv_o)
+        assert oracle.rel_l2(buf.cpu().numpy(), LU_o) < 1e-11
