@@ -838,6 +838,119 @@ static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const 
 
 static bool g_fft_tma_disabled() { return fft_knob("FB_FFT_NO_TMA", 0) == 1; }
 
+
+// =====================================================================================
+// Long rows (L = 16384, one line per CTA, 1024 threads): the padded exchange buffer alone is
+// 139 KB, so a second full staging buffer does not fit and the plain kernel leaves the SM idle
+// while each line loads.  This persistent kernel streams the NEXT line in two halves while the
+// current one is transformed: elements [0, L/2) go to a 64 KB staging buffer as soon as stage 1
+// has read it, elements [L/2, L) into the (dense) start of the exchange buffer once the last
+// exchange has been read.  Stage 1 reads the dense halves directly (thread t: k = t + 1024 m).
+// =====================================================================================
+template <bool OUT_GENERIC>
+__global__ void __launch_bounds__(1024, 1)
+    fft_longrow_kernel(const FftPass p, const float2* __restrict__ tw, const float2* __restrict__ stw) {
+    constexpr int LOG2L = 14;
+    using G = LineGeom<LOG2L>;
+    constexpr int L = G::L, T = G::T, E = G::E, H = L / 2;
+    extern __shared__ __align__(128) float2 smf[];
+    float2* X = smf;                  // [PADL] exchange; its first H elements also stage the second half
+    float2* S = smf + G::PADL;        // [H] first-half staging
+    uint64_t* bars = reinterpret_cast<uint64_t*>(S + H);
+    const int t = threadIdx.x;
+    const uint32_t bar_a = ptx::smem_u32(&bars[0]), bar_b = ptx::smem_u32(&bars[1]);
+    if (t == 0) {
+        ptx::mbar_init(bar_a, 1);
+        ptx::mbar_init(bar_b, 1);
+        ptx::fence_mbar_init();
+    }
+    __syncthreads();
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    auto line_src = [&](int64_t g) { return p.in + g * p.lin.hi; };
+    const int64_t nl = p.nlines;
+    int64_t g = blockIdx.x;
+    if (t == 0 && g < nl) {
+        ptx::mbar_arrive_expect_tx(bar_a, H * sizeof(float2));
+        ptx::bulk_load(ptx::smem_u32(S), line_src(g), H * sizeof(float2), bar_a);
+        ptx::mbar_arrive_expect_tx(bar_b, H * sizeof(float2));
+        ptx::bulk_load(ptx::smem_u32(X), line_src(g) + H, H * sizeof(float2), bar_b);
+    }
+    for (int it = 0; g < nl; g += gridDim.x, ++it) {
+        const int64_t gn = g + gridDim.x;
+        ptx::mbar_wait(bar_a, (uint32_t)it & 1u);
+        ptx::mbar_wait(bar_b, (uint32_t)it & 1u);
+        float2 v[E];
+#pragma unroll
+        for (int m = 0; m < E; ++m) v[m] = (m < E / 2) ? S[t + m * T] : X[t + (m - E / 2) * T];
+        if (p.conj_in) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
+        }
+        ptx::fence_proxy_async_smem();
+        __syncthreads();  // S and X consumed
+        if (t == 0 && gn < nl) {
+            ptx::mbar_arrive_expect_tx(bar_a, H * sizeof(float2));
+            ptx::bulk_load(ptx::smem_u32(S), line_src(gn), H * sizeof(float2), bar_a);
+        }
+        Stages<LOG2L, 1, 0>::run(v, X, t, 0, stw, nullptr);
+        ptx::fence_proxy_async_smem();
+        __syncthreads();  // the last exchange has been read
+        if (t == 0 && gn < nl) {
+            ptx::mbar_arrive_expect_tx(bar_b, H * sizeof(float2));
+            ptx::bulk_load(ptx::smem_u32(X), line_src(gn) + H, H * sizeof(float2), bar_b);
+        }
+        if (p.conj_out) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
+        }
+        if (p.scale != 1.0f) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) v[m] = __fmul2_rn(v[m], bc2(p.scale));
+        }
+        float2* dst = p.out + g * p.lout.hi;
+        if constexpr (!OUT_GENERIC) {
+#pragma unroll
+            for (int m = 0; m < E; ++m) dst[t + m * T] = v[m];
+        } else {
+            const int out_kmask = (1 << p.lout.kb_shift) - 1;
+#pragma unroll
+            for (int m = 0; m < E; ++m) {
+                const int k = t + m * T;
+                if (p.peer_out)
+                    p.peer[k >> p.lout.kb_shift][g * p.lout.hi + (int64_t)(k & out_kmask) * p.lout.es] = v[m];
+                else
+                    dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] = v[m];
+            }
+        }
+    }
+}
+
+static bool longrow_eligible(const FftPass& p) {
+    if (p.log2L != 14 || p.col_like || p.pair_log2N || p.peer_in || p.tw4_log2N || p.lin.lo || p.lout.lo) return false;
+    if (p.g_shift != 0 && p.g_shift < 62) return false;
+    if (p.lin.es != 1 || p.lin.kb_shift < 14 || p.lout.es != 1) return false;
+    if (((uintptr_t)p.in & 15) || ((uintptr_t)p.out & 15) || (p.lin.hi * 8) % 16) return false;
+    return fft_knob("FB_FFT_LONGROW", 1) != 0 && !g_fft_tma_disabled();
+}
+
+template <bool OG>
+static fb_status launch_longrow(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    using G = LineGeom<14>;
+    constexpr size_t SMEM = (size_t)(G::PADL + G::L / 2) * sizeof(float2) + 64;
+    static int attr_mask = 0;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (!(attr_mask & (1 << (dev & 31)))) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(fft_longrow_kernel<OG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
+        attr_mask |= 1 << (dev & 31);
+    }
+    int64_t grid = st->sm_count;
+    if (grid > p.nlines) grid = p.nlines;
+    return launch_pdl(fft_longrow_kernel<OG>, dim3((unsigned)grid), dim3(1024), SMEM, s, p,
+                      (const float2*)st->twiddles, (const float2*)st->stage_tw);
+}
+
 // All launches of one line length (explicitly instantiated per length in fb_fft_k*.cu so the
 // kernel variants compile in parallel translation units).
 template <int LOG2L>
@@ -861,6 +974,10 @@ fb_status launch_pass_L(const FftPass& p, const DeviceState* st, cudaStream_t s)
     }
     if constexpr (has_tma) {
         if (!g_fft_tma_disabled() && tma_eligible(p, kind, tc, og)) return launch_tma_L<LOG2L>(p, kind, tc, og, st, s);
+    }
+    if constexpr (LOG2L == 14) {
+        if (longrow_eligible(p))
+            return p.lout.kb_shift >= 14 && !p.peer_out ? launch_longrow<false>(p, st, s) : launch_longrow<true>(p, st, s);
     }
     return launch_L<LOG2L>(p, pick_C(LOG2L, p.col_like != 0), st, s);
 }
