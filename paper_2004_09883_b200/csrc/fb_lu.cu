@@ -227,7 +227,7 @@ template <int PT, int RPT, int PNB>
 __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid, int j0, int jb, int n,
                                                  int32_t* __restrict__ ipiv, int32_t* __restrict__ info) {
     constexpr int NW = PT / 32;
-    __shared__ double red_row[2][NW][PNB];  // each warp's candidate row
+    __shared__ __align__(16) double red_row[2][NW][PNB];  // each warp's candidate row
     __shared__ unsigned long long red_k[2][NW];
     __shared__ int red_r[2][NW];
     __shared__ double crow[2][PNB];
@@ -235,6 +235,9 @@ __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid,
 #pragma unroll
     for (int k = 0; k < PNB; ++k) {
         if (k >= jb) break;
+#ifdef FB_LU_TIMING
+        long long c0 = clock64();
+#endif
         const int par = k & 1;
         const int c = j0 + k;
         double bv = -1.0;
@@ -261,12 +264,21 @@ __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid,
         unsigned mhi = __reduce_max_sync(0xffffffffu, khi);
         unsigned mlo = __reduce_max_sync(0xffffffffu, khi == mhi ? klo : 0u);
         const int wr = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? br : INT_MAX));
-        if (br == wr && wr != INT_MAX) {
-#pragma unroll
-            for (int i = 0; i < RPT; ++i)
-                if (i == bi)
-#pragma unroll
-                    for (int j = 0; j < PNB; ++j) red_row[par][warp][j] = a[i][j];
+        if (br == wr && wr != INT_MAX) {  // one lane per warp: a real branch per row, 16-byte stores
+            double2* dst = reinterpret_cast<double2*>(&red_row[par][warp][0]);
+            switch (bi) {
+#define FB_LU_PUB(I)                                                                      \
+    case I:                                                                               \
+        if constexpr (I < RPT) {                                                          \
+            _Pragma("unroll") for (int j = 0; j < PNB; j += 2) dst[j / 2] = make_double2(a[I][j], a[I][j + 1]); \
+        }                                                                                 \
+        break;
+                FB_LU_PUB(0)
+                FB_LU_PUB(1)
+                FB_LU_PUB(2)
+                FB_LU_PUB(3)
+#undef FB_LU_PUB
+            }
         }
         if (lane == 0) {
             red_k[par][warp] = ((unsigned long long)mhi << 32) | mlo;
@@ -275,7 +287,13 @@ __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid,
         if (tid == k)
 #pragma unroll
             for (int j = 0; j < PNB; ++j) crow[par][j] = a[0][j];  // row c = j0 + k is thread k's row 0
+#ifdef FB_LU_TIMING
+        long long c1 = clock64();
+#endif
         __syncthreads();
+#ifdef FB_LU_TIMING
+        long long c2 = clock64();
+#endif
         key = (lane < NW) ? red_k[par][lane] : 0ull;
         const int rw = (lane < NW) ? red_r[par][lane] : INT_MAX;
         khi = (unsigned)(key >> 32);
@@ -285,6 +303,9 @@ __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid,
         const int p = (int)__reduce_min_sync(0xffffffffu, (unsigned)((khi == mhi && klo == mlo) ? rw : INT_MAX));
         if (tid == 0) ipiv[c] = p;
         const int op = (p - j0) % PT, ip = (p - j0) / PT;
+#ifdef FB_LU_TIMING
+        long long c3 = clock64();
+#endif
         double pr[PNB];
 #pragma unroll
         for (int j = 0; j < PNB; ++j) pr[j] = red_row[par][op >> 5][j];
@@ -300,6 +321,9 @@ __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid,
                         for (int j = 0; j < PNB; ++j) a[i][j] = crow[par][j];
             }
         }
+#ifdef FB_LU_TIMING
+        long long c4 = clock64();
+#endif
         const double piv = pr[k];
         if (piv == 0.0) {
             if (tid == 0 && *info == 0) *info = c + 1;
@@ -333,6 +357,12 @@ __device__ __forceinline__ void lu_panel_columns(double (&a)[RPT][PNB], int tid,
                 }
             }
         }
+#ifdef FB_LU_TIMING
+        long long c5 = clock64();
+        if ((tid == 0 || tid == 511) && (j0 == 80 || j0 == 1600) && k == 3)
+            printf("LU_COL tid=%d j0=%d scan+redux=%lld bar=%lld xwarp=%lld rows+swap=%lld update=%lld\n", tid, j0,
+                   c1 - c0, c2 - c1, c3 - c2, c4 - c3, c5 - c4);
+#endif
     }
 }
 
