@@ -171,8 +171,12 @@ fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void*
  * aligned, lda even): L unit lower (strictly below the diagonal), U upper.  LAPACK getrf
  * pivoting: at step k the pivot is the FIRST row p >= k of largest |A[p][k]|; whole rows are
  * swapped; ipiv[k] = p (device int32[n], 0-based).  *info (device int32) = 0, or k+1 for the
- * first exactly-zero pivot (that step is skipped, as LAPACK).  dtype FB_F64 only; n <= 4096.
- * ws: fb_lu_workspace_bytes(dtype, n) bytes (currently 0). */
+ * first exactly-zero pivot (that step is skipped, as LAPACK).  Multipliers are formed with the
+ * pivot's reciprocal when |pivot| >= DBL_MIN (dgetf2's sfmin rule).  dtype FB_F64 only;
+ * n <= 4096.  ws: fb_lu_workspace_bytes(dtype, n) bytes (currently 0).
+ * Execution: a look-ahead schedule on the caller's stream and an internal per-thread stream
+ * (joined back before return, in stream order), captured on first use for each (A, n, lda,
+ * ipiv, info) into a cached CUDA graph and replayed on later calls with the same buffers. */
 size_t fb_lu_workspace_bytes(int dtype, int64_t n);
 fb_status fb_lu(int dtype, int64_t n, void* A, int64_t lda, int32_t* ipiv, int32_t* info, void* ws,
                 size_t ws_bytes, void* stream);
