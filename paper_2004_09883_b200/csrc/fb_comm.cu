@@ -31,6 +31,9 @@ struct fb_comm {
     size_t win_bytes = 0;
     ncclWindow_t win = nullptr;
     float2* peer_base[fb::kMaxPeers] = {};  // window bases of every rank, as mapped here
+    // row-block GEMM: panel broadcasts run on their own stream
+    cudaStream_t cstream = nullptr;
+    cudaEvent_t cev = nullptr;
 };
 
 namespace fb {
@@ -292,6 +295,8 @@ fb_status fb_comm_destroy(fb_comm* c) {
         if (ncclMemFree(c->win_buf) != ncclSuccess) st = FB_ERR_NCCL;
         c->win_buf = nullptr;
     }
+    if (c->cev) cudaEventDestroy(c->cev);
+    if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->nccl && c->devcomm_ok) {
         if (ncclDevCommDestroy(c->nccl, &c->devcomm) != ncclSuccess) st = FB_ERR_NCCL;
         c->devcomm_ok = false;
@@ -461,9 +466,47 @@ fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_
         return FB_ERR_INVALID_VALUE;
     }
     const ncclDataType_t t = dtype == FB_F64 ? ncclDouble : ncclFloat;
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t ml = m / c->size;
+    const char* pk_s = getenv("FB_ROWBLOCK_PANEL");  // K rows per broadcast panel (FP32 path)
+    const int64_t pk = pk_s ? atoll(pk_s) : 4096;
+    if (dtype == FB_F32 && pk > 0 && pk < k) {
+        // B is broadcast in contiguous K-row panels on a communication stream;
+        // the operand split of A runs meanwhile, and each B panel is split (transposed to
+        // K-major hi/lo) as soon as its broadcast has landed, then the tensor-core GEMM runs.
+        const size_t need = gemm_ws_bytes(dtype, ml, n, k);
+        if (!ws || ws_bytes < need || !aligned16(ws) || !aligned16(A_rows) || !aligned16(B) || !aligned16(C_rows) ||
+            (lda * 4) % 16 || (ldc * 4) % 16 || (n * 4) % 16 || lda < k || ldc < n) {
+            set_error("row-block GEMM: operands / workspace (%zu bytes) invalid", need);
+            return FB_ERR_INVALID_VALUE;
+        }
+        DeviceState* st;
+        FB_TRY(ensure_device(nullptr, &st));
+        if (!c->cstream) {
+            FB_CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+            FB_CUDA_TRY(cudaEventCreateWithFlags(&c->cev, cudaEventDisableTiming));
+        }
+        const int64_t kp = (k + 3) / 4 * 4;
+        float* Ah = (float*)ws;
+        float* Al = Ah + ml * kp;
+        float* Bh = Al + ml * kp;
+        float* Bl = Bh + n * kp;
+        FB_CUDA_TRY(cudaEventRecord(c->cev, s));  // the broadcasts start after everything before the call
+        FB_CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->cev, 0));
+        FB_TRY(tf32_split_device(0, ml, k, (const float*)A_rows, lda, Ah, Al, kp, st, s));
+        for (int64_t p0 = 0; p0 < k; p0 += pk) {
+            const int64_t rows = (k - p0) < pk ? (k - p0) : pk;
+            float* Bp = (float*)B + p0 * n;
+            FB_NCCL_TRY(ncclBroadcast(Bp, Bp, (size_t)rows * (size_t)n, t, root, c->nccl, c->cstream), c->nccl);
+            FB_CUDA_TRY(cudaEventRecord(c->cev, c->cstream));
+            FB_CUDA_TRY(cudaStreamWaitEvent(s, c->cev, 0));  // binds to this panel's record
+            FB_TRY(tf32_split_device(1, rows, n, Bp, n, Bh + p0, Bl + p0, kp, st, s));
+        }
+        return gemm_3xtf32_presplit_device(ml, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C_rows, ldc, s);
+    }
     // B broadcast from root (in place on root) -- the only data exchange of the row-block GEMM
-    FB_NCCL_TRY(ncclBroadcast(B, B, (size_t)k * (size_t)n, t, root, c->nccl, (cudaStream_t)stream), c->nccl);
-    return fb_matmul(dtype, m / c->size, n, k, A_rows, lda, B, ldb, C_rows, ldc, ws, ws_bytes, stream);
+    FB_NCCL_TRY(ncclBroadcast(B, B, (size_t)k * (size_t)n, t, root, c->nccl, s), c->nccl);
+    return fb_matmul(dtype, ml, n, k, A_rows, lda, B, ldb, C_rows, ldc, ws, ws_bytes, stream);
 }
 
 }  // extern "C"

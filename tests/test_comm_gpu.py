@@ -146,3 +146,20 @@ def test_fused_model_vs_oracle(env):
     fb.fb_fft2d_slab_model(P, x, y, n0, n1)
     torch.cuda.synchronize()
     assert oracle.rel_l2(_assemble(y, P, n0, n1).cpu().numpy(), oracle.dft2d(xh)) < 5e-7
+
+
+@pytest.mark.parametrize("panel", ["64", "100", "0"])
+def test_rowblock_panel_broadcast_world1(env, panel, monkeypatch):
+    """The FP32 row-block GEMM broadcasts B in K-row panels on its own stream and splits each
+    panel as it lands; the product is bitwise the plain fb_matmul product
+    (same split arithmetic, same tensor-core kernel), ragged last panel included."""
+    fb, comm = env
+    monkeypatch.setenv("FB_ROWBLOCK_PANEL", panel)
+    m, n, k = 256, 192, 300
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).cuda()
+    B = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).cuda()
+    C = torch.empty(m, n, device="cuda")
+    comm.fb_matmul_rowblock(A, B, C, root=0)
+    ref = fb.matmul(A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
