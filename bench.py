@@ -432,6 +432,23 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                                            "frac": ach / pk["hbm_gbs"],
                                            "note": f"{passes} HBM passes x (R+W) of the 2 GiB array"}}
         del x, y, ws
+    if want("gemm_bf16_8192"):  # N4: BF16 operands, FP32 accumulation (roofline: measured BF16 peak)
+        n = 8192
+        g = torch.Generator(device="cuda").manual_seed(200409885)
+        A = (torch.rand(n, n, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+        Bt = (torch.rand(n, n, device="cuda", generator=g) * 2 - 1).to(torch.bfloat16)
+        C = torch.empty(n, n, device="cuda")
+        ms = timed_steps(torch, lambda: fb.matmul_bf16(A, Bt, b_transposed=True, out=C, stream=stream), steps,
+                         args.warmup, flush, stream)
+        t = float(np.mean(ms))
+        tf = 2.0 * n ** 3 / (t * 1e-3) / 1e12
+        res["gemm_bf16_8192"] = {"value": tf, "unit": "TFLOP/s", "ms_per_step": t,
+                                 "config": {"workload": "gemm_8192^3_bf16_fp32acc", "survey_next": "N4",
+                                            "b_layout": "K-major (B^T given)"},
+                                 "roofline": {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops"],
+                                              "unit": "TFLOP/s", "frac": tf / pk["bf16_tflops"],
+                                              "peak_source": pk["source"] + " (BF16 burst)"}}
+        del A, Bt, C
     if want("gemm_f32_32768"):  # configs[4] at 1 GPU: the scaling baseline of the row-block GEMM
         res["gemm_f32_32768"] = rowblock_gemm(args, torch, fb, np, stream, flush, pk, None, 0, 1, None)
     return res

@@ -118,6 +118,16 @@ fb_status fb_irfft2d(const void* y, void* x, int64_t n0, int64_t n1, void* ws, s
  * split operands; FP64: 0).  C must not overlap A, B or ws. */
 size_t fb_matmul_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k);
 
+/* BF16 GEMM: C[m][n] (float32) = A[m][k] * op(B), A and B bfloat16 (raw
+ * 16-bit storage), exact BF16 products accumulated in FP32 on tcgen05 (kind::f16, CTA pairs),
+ * partial sums promoted to round-to-nearest FP32 registers every 256 k.  b_transposed = 1: B is
+ * given K-major as [n][k] (ldb >= k); 0: B is [k][n] (ldb >= n) and is transposed into ws.
+ * A, B, C 16-byte aligned; lda*2, ldb*2, ldc*4 multiples of 16.  ws:
+ * fb_matmul_bf16_workspace_bytes(b_transposed, m, n, k) bytes (0 when b_transposed). */
+size_t fb_matmul_bf16_workspace_bytes(int b_transposed, int64_t m, int64_t n, int64_t k);
+fb_status fb_matmul_bf16(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                         int b_transposed, void* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream);
+
 /* BLAS-style variant: C = alpha op(A) op(B) + beta C, op(X) = X (trans 0) or
  * X^T (trans 1); op(A) is m x k (A stored m x k, lda >= k; or k x m, lda >= m), op(B) is k x n
  * (B stored k x n, ldb >= n; or n x k, ldb >= k).  Same arithmetic and accuracy as fb_matmul

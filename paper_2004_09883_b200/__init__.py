@@ -29,6 +29,7 @@ EXPORTS = [
     "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_init",
     "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d", "fb_fft1d_batched", "fb_ifft1d_batched",
     "fb_gemm_workspace_bytes", "fb_gemm", "fb_rfft2d_workspace_bytes", "fb_rfft2d", "fb_irfft2d",
+    "fb_matmul_bf16_workspace_bytes", "fb_matmul_bf16",
     "fb_matmul_workspace_bytes", "fb_matmul", "fb_tf32_split", "fb_matmul_3xtf32_presplit",
     "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
@@ -73,6 +74,8 @@ def lib() -> ctypes.CDLL:
         "fb_ifft1d_batched": ([vp, vp, i64, i64, vp], ci),
         "fb_matmul_workspace_bytes": ([ci, i64, i64, i64], sz),
         "fb_gemm_workspace_bytes": ([ci, ci, ci, i64, i64, i64], sz),
+        "fb_matmul_bf16_workspace_bytes": ([ci, i64, i64, i64], sz),
+        "fb_matmul_bf16": ([i64, i64, i64, vp, i64, vp, i64, ci, vp, i64, vp, sz, vp], ci),
         "fb_gemm": ([ci, ci, ci, i64, i64, i64, ctypes.c_double, vp, i64, vp, i64, ctypes.c_double, vp, i64, vp,
                      sz, vp], ci),
         "fb_matmul": ([ci, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], ci),
@@ -214,6 +217,21 @@ def ifft2d(x: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> tor
 
 
 # ------------------------------------------------------------------ matrix block
+def matmul_bf16(A: torch.Tensor, B: torch.Tensor, b_transposed: bool = False, out: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+    """float32 C = A @ B for bfloat16 A [m, k] and B [k, n] (or B^T [n, k] when b_transposed)."""
+    if A.dtype != torch.bfloat16 or B.dtype != torch.bfloat16:
+        raise ValueError("matmul_bf16 expects bfloat16 operands")
+    m, k = A.shape
+    n = B.shape[0] if b_transposed else B.shape[1]
+    C = torch.empty(m, n, dtype=torch.float32, device=A.device) if out is None else out
+    ws = _workspace_named(lib().fb_matmul_bf16_workspace_bytes(int(b_transposed), m, n, k), A.device, "bf16")
+    _check("fb_matmul_bf16", lib().fb_matmul_bf16(m, n, k, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
+                                                  int(b_transposed), _ptr(C), C.stride(0), _ptr(ws), ws.numel(),
+                                                  _stream(stream)))
+    return C
+
+
 def gemm(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, alpha: float = 1.0, beta: float = 0.0,
          trans_a: bool = False, trans_b: bool = False, stream=None) -> torch.Tensor:
     """C = alpha op(A) op(B) + beta C (fb_gemm); float32 (3xTF32) or float64 (DMMA)."""

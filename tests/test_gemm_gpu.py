@@ -198,3 +198,17 @@ def test_gemm_path_variants(fb, knobs, dt, monkeypatch):
     torch.cuda.synchronize()
     bar = 1e-5 if dt == torch.float32 else 1e-12
     assert oracle.rel_l2(C.cpu().numpy(), oracle.matmul(A.cpu().numpy(), B.cpu().numpy())) < bar
+
+
+@pytest.mark.parametrize("m,n,k,bt", [(256, 256, 64, True), (300, 200, 136, False), (512, 768, 1000, True),
+                                      (2048, 2048, 2048, False), (40, 24, 8, True)])
+def test_gemm_bf16_vs_oracle(fb, m, n, k, bt):
+    """fb_matmul_bf16: the product of the bf16 inputs (exact in FP64) within 1e-5
+    (FP32 accumulation, RN promotion every 256 k)."""
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(torch.bfloat16).cuda()
+    Bk = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).to(torch.bfloat16).cuda()
+    B = Bk.t().contiguous() if bt else Bk
+    C = fb.matmul_bf16(A, B, b_transposed=bt)
+    torch.cuda.synchronize()
+    ref = oracle.matmul(A.float().cpu().numpy().astype(np.float64), Bk.float().cpu().numpy().astype(np.float64))
+    assert oracle.rel_l2(C.cpu().numpy(), ref) < 1e-5
