@@ -35,7 +35,12 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     tn = in / gm;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
+// CL = 2: one CTA pair per 256 x 256 tile.  CL = 4: a cluster of two pairs computing the tiles
+// (m0, n0) and (m0, n0 + 256): the A half-tiles they share are loaded once and multicast to
+// both pairs (halving A's L2 -> SM traffic); every stage is released only when both pairs'
+// MMAs have consumed it (commits multicast to all four CTAs).
+template <int CL>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_bf16_pair_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                           float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n) {
     extern __shared__ uint8_t smem_raw[];
@@ -52,11 +57,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         reinterpret_cast<const uint32_t*>(smem + STAGES * STAGE_BYTES + 8 * (2 * STAGES + 4));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = ptx::cluster_ctarank();
+    const uint32_t crank = ptx::cluster_ctarank();
+    const uint32_t rank = crank & 1u, pair = crank >> 1;
     const bool leader = rank == 0;
     int tm, tn;
-    tile_coords(blockIdx.x >> 1, tiles_m, tiles_n, tm, tn);
+    if (CL == 2) {
+        tile_coords(blockIdx.x >> 1, tiles_m, tiles_n, tm, tn);
+    } else {
+        tile_coords(blockIdx.x >> 2, tiles_m, (tiles_n + 1) >> 1, tm, tn);
+        tn = 2 * tn + (int)pair;
+    }
     const int m0 = tm * 256, n0 = tn * 256;
+    const uint16_t own_pair_mask = (uint16_t)(0x3u << (2 * pair));
+    const uint16_t stage_mask = CL == 2 ? (uint16_t)0x3 : (uint16_t)0xF;
     const int KB = (K + BK - 1) / BK;
     const int NCHUNK = (KB + KP_BLOCKS - 1) / KP_BLOCKS;
 
@@ -65,7 +78,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         ptx::tma_prefetch_desc(&tmB);
         for (int s = 0; s < STAGES; ++s) {
             ptx::mbar_init(full_bar(s), 1);
-            ptx::mbar_init(empty_bar(s), 1);
+            ptx::mbar_init(empty_bar(s), CL / 2);  // one commit per pair of the cluster
         }
         for (int b = 0; b < 2; ++b) {
             ptx::mbar_init(tfull_bar(b), 1);
@@ -93,7 +106,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * STAGE_BYTES);
                 const uint32_t st = base + s * STAGE_BYTES;
                 const int kc = kb * BK;
-                ptx::tma_load_2d_pair(st, &tmA, full_bar(s), kc, am);
+                if (CL == 2)
+                    ptx::tma_load_2d_pair(st, &tmA, full_bar(s), kc, am);
+                else if (pair == 0)  // A half `rank` for both pairs (CTAs rank and rank + 2)
+                    ptx::tma_load_2d_pair_mc(st, &tmA, full_bar(s), kc, am, (uint16_t)((1u << rank) | (4u << rank)));
                 ptx::tma_load_2d_pair(st + TILE_BYTES, &tmB, full_bar(s), kc, bn);
             }
         }
@@ -122,9 +138,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                         const uint64_t b = ptx::smem_desc_sw128_kmajor(st + TILE_BYTES + off);
                         ptx::mma_f16_pair(tmem_d, a, b, idesc, (kb > c * KP_BLOCKS || kk > 0) ? 1u : 0u);
                     }
-                    ptx::mma_commit_pair(empty_bar(s), 0x3);
+                    ptx::mma_commit_pair(empty_bar(s), stage_mask);
                 }
-                ptx::mma_commit_pair(tfull_bar(buf), 0x3);
+                ptx::mma_commit_pair(tfull_bar(buf), own_pair_mask);
             }
         }
     } else {  // epilogue warps 2..9: lanes 32*(warp%4), column half (warp-2)/4
@@ -278,32 +294,46 @@ fb_status fb_matmul_bf16(int64_t m, int64_t n, int64_t k, const void* A, int64_t
     CUtensorMap mA, mB;
     FB_TRY(bf16::kmajor_map(&mA, A, m, k, lda));
     FB_TRY(bf16::kmajor_map(&mB, Bt, n, k, ldbt));
+    // A/B knob FB_BF16_CLUSTER=4: two pairs per cluster with the A tiles multicast (correct, but
+    // measured slower at 8192^3: 1227 vs 1312 TFLOP/s -- operand traffic is not the limit)
+    const char* ck = getenv("FB_BF16_CLUSTER");
+    const int CLn = (ck && ck[0] == '4') ? 4 : 2;
     static int attr_mask = 0;
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_mask & (1 << (dev & 31)))) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(bf16::gemm_bf16_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        FB_CUDA_TRY(cudaFuncSetAttribute(bf16::gemm_bf16_pair_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)bf16::SMEM));
+        FB_CUDA_TRY(cudaFuncSetAttribute(bf16::gemm_bf16_pair_kernel<4>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)bf16::SMEM));
         attr_mask |= 1 << (dev & 31);
     }
     const int tiles_m = (int)((m + 255) / 256), tiles_n = (int)((n + 255) / 256);
-    const int64_t tiles = (int64_t)tiles_m * tiles_n;
-    if (2 * tiles > INT32_MAX) {
+    const int64_t ctas = CLn == 2 ? 2 * (int64_t)tiles_m * tiles_n : 4 * (int64_t)tiles_m * ((tiles_n + 1) / 2);
+    if (ctas > INT32_MAX) {
         set_error("too many tiles");
         return FB_ERR_UNSUPPORTED_SIZE;
     }
     cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(2 * tiles));
+    cfg.gridDim = dim3((unsigned)ctas);
     cfg.blockDim = dim3(bf16::NUM_THREADS);
     cfg.dynamicSmemBytes = bf16::SMEM;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[0].val.programmaticStreamSerializationAllowed = 1;
+    attr[1].id = cudaLaunchAttributeClusterDimension;
+    attr[1].val.clusterDim.x = CLn;
+    attr[1].val.clusterDim.y = 1;
+    attr[1].val.clusterDim.z = 1;
     cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, bf16::gemm_bf16_pair_kernel, mA, mB, (float*)C, (int)m, (int)n, (int)k, ldc,
-                                   tiles_m, tiles_n));
+    cfg.numAttrs = 2;
+    if (CLn == 2)
+        FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, bf16::gemm_bf16_pair_kernel<2>, mA, mB, (float*)C, (int)m, (int)n, (int)k,
+                                       ldc, tiles_m, tiles_n));
+    else
+        FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, bf16::gemm_bf16_pair_kernel<4>, mA, mB, (float*)C, (int)m, (int)n, (int)k,
+                                       ldc, tiles_m, tiles_n));
     FB_LAUNCH_CHECK("gemm_bf16_pair_kernel");
     return FB_OK;
 }

@@ -212,3 +212,16 @@ def test_gemm_bf16_vs_oracle(fb, m, n, k, bt):
     torch.cuda.synchronize()
     ref = oracle.matmul(A.float().cpu().numpy().astype(np.float64), Bk.float().cpu().numpy().astype(np.float64))
     assert oracle.rel_l2(C.cpu().numpy(), ref) < 1e-5
+
+
+def test_gemm_bf16_multicast_cluster(fb, monkeypatch):
+    """The 4-CTA cluster variant (A tiles multicast to two CTA pairs) gives the same product
+    bit for bit (same MMA order per tile), including an odd tile count along N."""
+    m, n, k = 512, 768, 640
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(torch.bfloat16).cuda()
+    Bt = torch.from_numpy(synth.real_matrix(n, k, synth.TID_GEMM_B)).to(torch.bfloat16).cuda()
+    C2 = fb.matmul_bf16(A, Bt, b_transposed=True)
+    monkeypatch.setenv("FB_BF16_CLUSTER", "4")
+    C4 = fb.matmul_bf16(A, Bt, b_transposed=True)
+    torch.cuda.synchronize()
+    assert torch.equal(C2, C4)
