@@ -1,6 +1,6 @@
 cd $GRAFT_REPO_ROOT
 rm -f gpurun_out/sweep.jsonl
-for cfg in "" "FB_FFT_COL_MAX_LOG2=10" "FB_FFT_COL_MAX_LOG2=10 FB_FFT_4STEP_LB=4" "FB_FFT_COL_MAX_LOG2=10 FB_FFT_4STEP_LB=5" "FB_FFT_COL_MAX_LOG2=10 FB_FFT_4STEP_LB=7" "FB_FFT_COL_MAX_LOG2=10 FB_FFT_4STEP_LB=3"; do
+for cfg in "" "FB_FFT_GRID_WAVES=3" "FB_FFT_GRID_WAVES=4" "FB_FFT_GRID_WAVES=3 FB_FFT_COL_NB=2 FB_FFT_ROW_NB=2"; do
 env $cfg timeout 60 python tools/fft_pass_bench.py 2048 2048 40 | sed "s/}}/, \"cfg\": \"$cfg\"}}/" >> gpurun_out/sweep.jsonl 2>&1
+env $cfg timeout 60 python tools/fft_pass_bench.py 16384 16384 10 | sed "s/}}/, \"cfg\": \"$cfg\"}}/" >> gpurun_out/sweep.jsonl 2>&1
 done
-FB_FFT_COL_MAX_LOG2=10 FB_FFT_4STEP_LB=5 timeout 120 ncu --metrics gpu__time_duration.sum --cache-control none --clock-control none --csv --log-file gpurun_out/fs.csv python tools/fft_pass_bench.py 2048 2048 3 > /dev/null 2>&1
