@@ -225,3 +225,23 @@ def test_gemm_bf16_multicast_cluster(fb, monkeypatch):
     C4 = fb.matmul_bf16(A, Bt, b_transposed=True)
     torch.cuda.synchronize()
     assert torch.equal(C2, C4)
+
+
+def test_config4_full_size_sampled(fb):
+    """configs[4] at its full size (32768^3 FP32, the launch configuration bench.py times at one
+    GPU): sampled full rows and columns of C against the oracle (each 2^30 FP64 MACs)."""
+    n = 32768
+    g = torch.Generator(device="cuda").manual_seed(200409883)
+    A = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    B = torch.rand(n, n, device="cuda", generator=g) * 2 - 1
+    C = fb.matmul(A, B)
+    torch.cuda.synchronize()
+    Ah, Bh = A.cpu().numpy(), B.cpu().numpy()
+    rows, cols = [0, 12345, n - 1], [0, 777, n - 1]
+    Ch = C.cpu().numpy()
+    del A, B, C
+    torch.cuda.empty_cache()
+    err_r = oracle.rel_l2(Ch[rows], oracle.matmul_rows(Ah, Bh, rows))
+    err_c = oracle.rel_l2(Ch[:, cols].T, oracle.matmul_cols(Ah, Bh, cols))
+    print(f"32768^3 3xTF32 sampled rel-L2 rows {err_r:.3e} cols {err_c:.3e}")
+    assert err_r < 1e-5 and err_c < 1e-5
