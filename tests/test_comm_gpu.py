@@ -163,3 +163,25 @@ def test_rowblock_panel_broadcast_world1(env, panel, monkeypatch):
     ref = fb.matmul(A, B)
     torch.cuda.synchronize()
     assert torch.equal(C, ref)
+
+
+def test_fused_model_config3_full_size(env):
+    """configs[3] at its full size: the fused slab transpose's addressing for P = 2 and 8 virtual
+    ranks on the 16384^2 problem, bitwise against P = 1 (the same per-line kernels), and P = 1
+    against the single-GPU 2D FFT (different column plan: tolerance)."""
+    fb, comm = env
+    n = 16384
+    x = torch.from_numpy(synth.complex_field(n, n)).cuda()
+    y1 = torch.empty(n * n, dtype=torch.complex64, device="cuda")
+    fb.fb_fft2d_slab_model(1, x, y1, n, n)
+    y1 = y1.view(n, n)
+    for P in (2, 8):
+        y = torch.empty(n * n, dtype=torch.complex64, device="cuda")
+        fb.fb_fft2d_slab_model(P, x, y, n, n)
+        torch.cuda.synchronize()
+        assert torch.equal(_assemble(y, P, n, n), y1), P
+        del y
+    ref = fb.fft2d(x)
+    torch.cuda.synchronize()
+    d = (y1 - ref).abs().pow(2).sum().sqrt() / ref.abs().pow(2).sum().sqrt()
+    assert float(d) < 1e-6
