@@ -689,7 +689,9 @@ __global__ void __launch_bounds__(PT, 1)
         const int nbox = (mr + LU_BOXR - 1) / LU_BOXR;
         for (int q = 0; q < nbox; ++q) ptx::tma_store_2d(&tmA, ptx::smem_u32(P + q * LU_BOXR * PNB), j0, r0 + q * LU_BOXR);
         ptx::bulk_commit();
-        ptx::bulk_wait0();
+        // only the shared-memory source must outlive the CTA; the global writes are complete
+        // when the grid is (the next kernel depends on the grid, as a CUTLASS TMA epilogue)
+        ptx::bulk_wait_read0();
     }
 #ifdef FB_LU_TIMING
     __syncthreads();
