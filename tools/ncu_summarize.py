@@ -51,8 +51,8 @@ def main():
                 u = units[hdr.index(k)]
                 if label.endswith("_MB") and u in scale:  # normalise to MB whatever unit ncu chose
                     v = "%.3f" % (float(v.replace(",", "")) * scale[u])
-                elif k == "gpu__time_duration.sum" and u in ("ns", "msecond", "usecond", "nsecond"):
-                    f = {"ns": 1e-3, "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}[u]
+                elif k == "gpu__time_duration.sum" and u in ("ns", "us", "ms", "msecond", "usecond", "nsecond"):
+                    f = {"ns": 1e-3, "nsecond": 1e-3, "us": 1.0, "usecond": 1.0, "ms": 1e3, "msecond": 1e3}[u]
                     v = "%.3f" % (float(v.replace(",", "")) * f)
                 vals[label] = v
         lines.append("    " + "  ".join(f"{k}={v}" for k, v in vals.items()))
