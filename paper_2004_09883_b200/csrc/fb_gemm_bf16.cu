@@ -11,6 +11,10 @@
 #include "fb_common.cuh"
 #include "fb_ptx.cuh"
 
+#ifndef FB_BF16_GROUP_M
+#define FB_BF16_GROUP_M 8  // M tiles per rasterisation group (L2 reuse of the B panels)
+#endif
+
 namespace fb {
 namespace bf16 {
 constexpr int BK = 64;                                   // elements per k-block (128-byte rows)
@@ -23,7 +27,7 @@ constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t ACC_COLS = 256;
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;
 constexpr int KP_BLOCKS = 4;
-constexpr int GROUP_M = 8;
+constexpr int GROUP_M = FB_BF16_GROUP_M;
 
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
     const int per_group = GROUP_M * tiles_n;
