@@ -100,6 +100,8 @@ struct FftPass {
     int tw4_log2N;  // >0: four-step twiddle W_N^{(g >> g_shift) * k} on the output, N = 2^tw4_log2N
     int col_like;   // 1: adjacent lines are adjacent in memory (pick a wide C for coalescing)
     int debug;      // timing decomposition only (FB_FFT_DEBUG): 1 skip stages, 2 skip loads, 4 skip stores
+    int stagger_ns; // persistent TMA pass: CTA slot s (= blockIdx / SMs) delays its first load by s * this
+    int sm_count;   //   (set by launch_fft_pass)
     int pair_log2N; // >0: lines come in pairs (g = 2q + c, rows q and q + N/2 of an N-long column);
                     // after the row FFT, the radix-2 column butterfly across the pair and the
                     // four-step twiddle W_N^{q k_a} are applied (first step of a 2 x N/2 split)

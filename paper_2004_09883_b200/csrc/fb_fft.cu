@@ -26,6 +26,8 @@ fb_status launch_fft_pass(const FftPass& p_in, const DeviceState* st, cudaStream
     if (p_in.nlines <= 0) return FB_OK;
     FftPass p = p_in;
     p.debug = fft_knob("FB_FFT_DEBUG", 0);
+    p.stagger_ns = fft_knob("FB_FFT_STAGGER", 300);
+    p.sm_count = st->sm_count;
     switch (p.log2L) {
         case 0: return launch_pass_L<0>(p, st, s);
         case 1: return launch_pass_L<1>(p, st, s);
