@@ -646,7 +646,14 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m] = __fmul2_rn(v[m], bc2(p.scale));
         }
-        if constexpr (KIND == KIND_COL) {
+        if (KIND == KIND_COL && p.col_stg) {
+            // column results straight from registers (C-wide row segments per warp store)
+            const int64_t row = gh * p.lout.hi + (g & gmask) * p.lout.lo;
+            float2* dp = p.out + row + (int64_t)t * p.lout.es;
+            const int64_t step = (int64_t)T * p.lout.es;
+#pragma unroll
+            for (int m = 0; m < E; ++m) dp[m * step] = v[m];
+        } else if constexpr (KIND == KIND_COL) {
             __syncthreads();  // last stage finished reading X
             float2* xp = X + t * C + c;
 #pragma unroll
@@ -755,7 +762,14 @@ static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStr
             return FB_ERR_CUDA;
         }
     }
-    FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), TG::SMEM, s, p, tin, tout,
+    // Column outputs: direct stores from registers when a warp store covers whole 128-byte row
+    // segments (C = 16), else the exchange buffer + TMA tensor store (A/B, means of 3 x 100:
+    // 512^2 12.06 -> 11.36 us and 16384^2 2.892 -> 2.870 ms with direct stores; 2048^2
+    // (C = 4, 32-byte segments) 37.84 -> 40.13 us and 4096^2 157.7 -> 167.1 us, so those keep
+    // the TMA store).  Knob FB_FFT_COL_STG = 0 / 1 forces.
+    FftPass pk = p;
+    if (KIND == KIND_COL) pk.col_stg = (p.col_stg >= 0) ? p.col_stg : (C >= 16 ? 1 : 0);
+    FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), TG::SMEM, s, pk, tin, tout,
                       (const float2*)st->twiddles, (const float2*)st->stage_tw, ngroups, nh));
     return FB_OK;
 }
