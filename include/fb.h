@@ -169,6 +169,17 @@ fb_status fb_matmul_3xtf32_presplit(int64_t m, int64_t n, int64_t k, const float
 size_t fb_fft2d_host_workspace_bytes(int64_t n0, int64_t n1);
 fb_status fb_fft2d_host(const void* x_host, void* y_host, int64_t n0, int64_t n1, int inverse,
                         void* dev, size_t dev_bytes, void* stream);
+/* Streaming host form: `batch` independent n0 x n1 transforms, x_host/y_host hold them back to
+ * back (batch * n0 * n1 complex64 each, pinned for overlap).  Two device slots (dev: caller-owned
+ * DEVICE scratch of fb_fft2d_host_batch_workspace_bytes = 2 x the fb_fft2d_host scratch) alternate
+ * between `stream` and a library-owned auxiliary stream, so transform i+1's H2D copy overlaps
+ * transform i's D2H copy (PCIe is full duplex) with the kernels in between: the offload pipeline
+ * that hides the transfer overhead P:43 names.  Ordered after prior work on `stream`; returns
+ * after every result is in host memory.  Errors: as fb_fft2d_host; batch < 1 is
+ * FB_ERR_INVALID_VALUE.  Calls are serialised per process (one pipeline at a time). */
+size_t fb_fft2d_host_batch_workspace_bytes(int64_t n0, int64_t n1);
+fb_status fb_fft2d_host_batch(const void* x_host, void* y_host, int64_t n0, int64_t n1, int64_t batch,
+                              int inverse, void* dev, size_t dev_bytes, void* stream);
 size_t fb_matmul_host_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k);
 fb_status fb_matmul_host(int dtype, int64_t m, int64_t n, int64_t k, const void* A_host,
                          const void* B_host, void* C_host, void* dev, size_t dev_bytes,

@@ -31,7 +31,8 @@ EXPORTS = [
     "fb_gemm_workspace_bytes", "fb_gemm", "fb_rfft2d_workspace_bytes", "fb_rfft2d", "fb_irfft2d",
     "fb_matmul_bf16_workspace_bytes", "fb_matmul_bf16",
     "fb_matmul_workspace_bytes", "fb_matmul", "fb_tf32_split", "fb_matmul_3xtf32_presplit",
-    "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
+    "fb_fft2d_host_workspace_bytes", "fb_fft2d_host", "fb_fft2d_host_batch_workspace_bytes",
+    "fb_fft2d_host_batch", "fb_matmul_host_workspace_bytes", "fb_matmul_host",
     "fb_comm_unique_id_bytes", "fb_comm_unique_id", "fb_comm_init", "fb_comm_destroy", "fb_comm_rank",
     "fb_comm_size", "fb_fft2d_slab_workspace_bytes", "fb_fft2d_slab", "fb_ifft2d_slab",
     "fb_comm_fused", "fb_comm_fused_detail", "fb_fft2d_slab_model",
@@ -83,6 +84,8 @@ def lib() -> ctypes.CDLL:
         "fb_matmul_3xtf32_presplit": ([i64, i64, i64, vp, vp, i64, vp, vp, i64, vp, i64, vp], ci),
         "fb_fft2d_host_workspace_bytes": ([i64, i64], sz),
         "fb_fft2d_host": ([vp, vp, i64, i64, ci, vp, sz, vp], ci),
+        "fb_fft2d_host_batch_workspace_bytes": ([i64, i64], sz),
+        "fb_fft2d_host_batch": ([vp, vp, i64, i64, i64, ci, vp, sz, vp], ci),
         "fb_matmul_host_workspace_bytes": ([ci, i64, i64, i64], sz),
         "fb_matmul_host": ([ci, i64, i64, i64, vp, vp, vp, vp, sz, vp], ci),
         "fb_comm_unique_id_bytes": ([], sz),
@@ -320,6 +323,16 @@ def fb_fft2d_host(x_host: torch.Tensor, y_host: torch.Tensor, inverse: bool = Fa
     dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
     _check("fb_fft2d_host", lib().fb_fft2d_host(_ptr(x_host), _ptr(y_host), n0, n1, int(inverse), _ptr(dev),
                                                 dev.numel(), _stream(stream)))
+
+
+def fb_fft2d_host_batch(x_host: torch.Tensor, y_host: torch.Tensor, inverse: bool = False, device=0, stream=None):
+    """HOST complex64 [batch, n0, n1] in -> pipelined H2D / 2D FFT / D2H over two device slots
+    (copies of consecutive transforms overlap in both PCIe directions) -> HOST out (synchronous)."""
+    b, n0, n1 = x_host.shape
+    need = lib().fb_fft2d_host_batch_workspace_bytes(n0, n1)
+    dev = _workspace_named(need, torch.device("cuda", device), "host_batch_dev")
+    _check("fb_fft2d_host_batch", lib().fb_fft2d_host_batch(_ptr(x_host), _ptr(y_host), n0, n1, b, int(inverse),
+                                                            _ptr(dev), dev.numel(), _stream(stream)))
 
 
 def fb_matmul_host(A_host: torch.Tensor, B_host: torch.Tensor, C_host: torch.Tensor, device=0, stream=None):

@@ -78,6 +78,17 @@ static fb_status init_device_locked(int dev) {
     } else {
         st.twiddles = tw;
         st.stage_tw = stw;
+        if (cudaStreamCreateWithFlags(&st.aux, cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.ev_join, cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.ev_h2d[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.ev_h2d[1], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.ev_d2h[0], cudaEventDisableTiming) != cudaSuccess ||
+            cudaEventCreateWithFlags(&st.ev_d2h[1], cudaEventDisableTiming) != cudaSuccess) {
+            set_error("fb_init(%d): stream/event creation failed", dev);
+            cudaSetDevice(cur);
+            return FB_ERR_CUDA;
+        }
         st.sm_count = prop.multiProcessorCount;
         st.ready = true;
     }
@@ -374,6 +385,58 @@ fb_status fb_fft2d_host(const void* x_host, void* y_host, int64_t n0, int64_t n1
     FB_CUDA_TRY(cudaMemcpyAsync(d, x_host, bytes, cudaMemcpyHostToDevice, s));
     FB_TRY(fft2d_device(d, d, n0, n1, inverse != 0, ws, fft2d_ws_bytes(n0, n1), st, s));
     FB_CUDA_TRY(cudaMemcpyAsync(y_host, d, bytes, cudaMemcpyDeviceToHost, s));
+    FB_CUDA_TRY(cudaStreamSynchronize(s));
+    return FB_OK;
+}
+
+size_t fb_fft2d_host_batch_workspace_bytes(int64_t n0, int64_t n1) {
+    const size_t one = fb_fft2d_host_workspace_bytes(n0, n1);
+    return one ? 2 * round_up(one, 256) : 0;
+}
+
+// Streaming form of fb_fft2d_host: `batch` independent transforms x_host[i] -> y_host[i]
+// through two device slots, slot i % 2 on the caller's stream (even i) or the library's
+// auxiliary stream (odd i), so the H2D copy of transform i + 1 and the D2H copy of transform i
+// run on the two copy directions at once while the kernels run between them.  Ordered after
+// prior work on `stream`; returns after every result is in host memory.
+static std::mutex g_host_batch_mu;
+fb_status fb_fft2d_host_batch(const void* x_host, void* y_host, int64_t n0, int64_t n1, int64_t batch,
+                              int inverse, void* dev, size_t dev_bytes, void* stream) {
+    clear_error();
+    FB_TRY(check_fft_dims(n0, n1));
+    if (!x_host || !y_host || !dev || batch < 1) {
+        set_error(batch < 1 ? "batch must be >= 1" : "null pointer");
+        return FB_ERR_INVALID_VALUE;
+    }
+    const size_t need = fb_fft2d_host_batch_workspace_bytes(n0, n1);
+    if (dev_bytes < need || !aligned16(dev)) {
+        set_error("device scratch of %zu bytes (16B aligned) required, got %zu", need, dev_bytes);
+        return FB_ERR_WORKSPACE;
+    }
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    std::lock_guard<std::mutex> lk(g_host_batch_mu);  // one pipeline (aux stream, events) at a time
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)n0 * n1 * sizeof(float2);
+    const size_t slot = need / 2;
+    FB_CUDA_TRY(cudaEventRecord(st->ev_fork, s));
+    FB_CUDA_TRY(cudaStreamWaitEvent(st->aux, st->ev_fork, 0));
+    for (int64_t i = 0; i < batch; ++i) {
+        cudaStream_t ss = (i & 1) ? st->aux : s;
+        char* d = (char*)dev + (i & 1) * slot;
+        void* ws = d + round_up(bytes, 256);
+        // copies of one direction run one at a time, in transform order (each at the full link
+        // rate), so transform i's D2H overlaps transform i+1's H2D from the first pair on
+        if (i > 0) FB_CUDA_TRY(cudaStreamWaitEvent(ss, st->ev_h2d[(i - 1) & 1], 0));
+        FB_CUDA_TRY(cudaMemcpyAsync(d, (const char*)x_host + i * bytes, bytes, cudaMemcpyHostToDevice, ss));
+        FB_CUDA_TRY(cudaEventRecord(st->ev_h2d[i & 1], ss));
+        FB_TRY(fft2d_device(d, d, n0, n1, inverse != 0, ws, fft2d_ws_bytes(n0, n1), st, ss));
+        if (i > 0) FB_CUDA_TRY(cudaStreamWaitEvent(ss, st->ev_d2h[(i - 1) & 1], 0));
+        FB_CUDA_TRY(cudaMemcpyAsync((char*)y_host + i * bytes, d, bytes, cudaMemcpyDeviceToHost, ss));
+        FB_CUDA_TRY(cudaEventRecord(st->ev_d2h[i & 1], ss));
+    }
+    FB_CUDA_TRY(cudaEventRecord(st->ev_join, st->aux));
+    FB_CUDA_TRY(cudaStreamWaitEvent(s, st->ev_join, 0));
     FB_CUDA_TRY(cudaStreamSynchronize(s));
     return FB_OK;
 }

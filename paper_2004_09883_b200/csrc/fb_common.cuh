@@ -53,6 +53,9 @@ struct DeviceState {
     int sm_count = 0;
     float2* twiddles = nullptr;  // 16384 entries, W[j] = exp(-2 pi i j / 16384)
     float2* stage_tw = nullptr;  // per-(line length, stage) contiguous twiddles (fb_fft.cu)
+    cudaStream_t aux = nullptr;  // second slot of the host-batch copy/compute pipeline
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};  // copy-order chain
 };
 int64_t stage_tw_total();
 void stage_tw_index(int32_t* idx);

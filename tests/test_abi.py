@@ -56,6 +56,12 @@ def test_fft_validation_without_device(L):
     assert L.fb_fft2d_workspace_bytes(2048, 2048) == 2048 * 2048 * 8  # 2 x 1024 split plan
     assert L.fb_fft2d_workspace_bytes(8192, 64) == 8192 * 64 * 8
     assert L.fb_fft2d(p, ctypes.c_void_p(1 << 40), 8192, 64, None, 0, None) == 4
+    # streaming host form: batch >= 1, two slots of the fb_fft2d_host scratch, checked before any device work
+    one = L.fb_fft2d_host_workspace_bytes(2048, 2048)
+    assert L.fb_fft2d_host_batch_workspace_bytes(2048, 2048) == 2 * ((one + 255) // 256 * 256)
+    assert L.fb_fft2d_host_batch(p, p, 2048, 2048, 0, 0, p, 1 << 40, None) == 1
+    assert L.fb_fft2d_host_batch(p, p, 2048, 3000, 2, 0, p, 1 << 40, None) == 2
+    assert L.fb_fft2d_host_batch(p, p, 2048, 2048, 2, 0, p, one, None) == 4
 
 
 def test_matmul_validation_without_device(L):

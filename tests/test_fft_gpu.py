@@ -180,6 +180,25 @@ def test_host_variant(fb):
     assert oracle.rel_l2(xh.numpy(), x) < 5e-7
 
 
+@pytest.mark.parametrize("batch", [1, 2, 5])
+def test_host_batch_pipeline(fb, batch):
+    """Streaming host form: each transform of the batch equals the single-call result bit for
+    bit (same kernels, two device slots on two streams) and the oracle within the gate."""
+    n0, n1 = 512, 256
+    xs = np.stack([synth.complex_field(n0, n1, tensor_id=100 + i) for i in range(batch)])
+    xb = torch.from_numpy(xs).pin_memory()
+    yb = torch.empty_like(xb).pin_memory()
+    fb.fb_fft2d_host_batch(xb, yb)
+    yh = torch.empty(n0, n1, dtype=torch.complex64).pin_memory()
+    for i in range(batch):
+        fb.fb_fft2d_host(xb[i].contiguous().pin_memory(), yh)
+        assert np.array_equal(yb[i].numpy().view(np.uint32), yh.numpy().view(np.uint32))
+        assert oracle.rel_l2(yb[i].numpy(), oracle.dft2d(xs[i])) < 5e-7
+    zb = torch.empty_like(xb).pin_memory()
+    fb.fb_fft2d_host_batch(yb, zb, inverse=True)
+    assert oracle.rel_l2(zb.numpy(), xs) < 5e-7
+
+
 @pytest.mark.parametrize("n0,n1", [(64, 128), (1, 256), (256, 256)])
 def test_nr_fourn_shim(fb, n0, n1):
     """NR fourn conventions: 1-based data/nn, isign=-1 -> exp(-2 pi i), isign=+1 ->
@@ -285,7 +304,8 @@ def test_irfft2d_vs_oracle_inverse(fb):
 
 
 @pytest.mark.parametrize("knobs", [{"FB_FFT_NO_TMA": "1"}, {"FB_FFT_PAIR_TMA": "0"}, {"FB_FFT_ROW_NB": "2"},
-                                   {"FB_FFT_COL_NB": "2"}, {"FB_FFT_NO_PDL": "1"}, {"FB_FFT_COL_MAX_LOG2": "10"}])
+                                   {"FB_FFT_COL_NB": "2"}, {"FB_FFT_NO_PDL": "1"}, {"FB_FFT_COL_MAX_LOG2": "10"},
+                                   {"FB_FFT_COL_STG": "0"}, {"FB_FFT_COL_STG": "1"}, {"FB_FFT_STAGGER": "0"}])
 @pytest.mark.parametrize("n0,n1", [(512, 256), (2048, 128), (4096, 64)])
 def test_fft_path_variants_vs_oracle(fb, n0, n1, knobs, monkeypatch):
     """Each kernel path behind an A/B knob (no TMA, plain-kernel pair row pass, forced staging
@@ -299,6 +319,23 @@ def test_fft_path_variants_vs_oracle(fb, n0, n1, knobs, monkeypatch):
     torch.cuda.synchronize()
     assert oracle.rel_l2(y.cpu().numpy(), oracle.dft2d(xh)) < 5e-7
     assert oracle.rel_l2(z.cpu().numpy(), xh) < 5e-7
+
+
+@pytest.mark.parametrize("n0,n1", [(512, 512), (2048, 2048), (8192, 256)])
+def test_store_path_and_stagger_bitwise(fb, n0, n1, monkeypatch):
+    """The column-output path (exchange buffer + TMA store vs direct register stores) and the
+    staggered start change only how bytes move, not the arithmetic: results are bit-identical."""
+    xh = synth.complex_field(n0, n1)
+    x = torch.from_numpy(xh).cuda()
+    outs = []
+    for knobs in ({}, {"FB_FFT_COL_STG": "0"}, {"FB_FFT_COL_STG": "1"}, {"FB_FFT_STAGGER": "0"}):
+        for k in ("FB_FFT_COL_STG", "FB_FFT_STAGGER"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in knobs.items():
+            monkeypatch.setenv(k, v)
+        outs.append(fb.fft2d(x).cpu().numpy())
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
 
 
 def test_longrow_kernel_matches_plain_kernel(fb, monkeypatch):
