@@ -2,7 +2,7 @@
 // FP32 accumulation) on the 5th-generation tensor cores, the same CTA-pair design as the 3xTF32
 // kernel (fb_gemm.cu): TMA 128B-swizzled K-major tiles -> mbarrier ring -> one thread issues
 // tcgen05.mma.cta_group::2.kind::f16 (M = 256, N = 256, K = 16 per instruction) -> double-
-// buffered TMEM accumulators drained every 4 k-blocks into RN FP32 registers -> C.  B must be
+// buffered TMEM accumulators drained every 16 k-blocks (1024 k) into RN FP32 registers -> C.  B must be
 // K-major ([n][k], i.e. B transposed); a row-major [k][n] B is transposed in the workspace.
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -26,7 +26,13 @@ constexpr uint32_t STAGE_BYTES = 2 * TILE_BYTES;         // A half, B half
 constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t ACC_COLS = 256;
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;
-constexpr int KP_BLOCKS = 4;
+// k-blocks (of 64) between TMEM drains into RN FP32 registers: every 1024 k (A/B at 8192^3:
+// 256 k 0.842 ms, 512 k 0.790 ms, 1024 k 0.785 ms; the truncating TMEM accumulation then
+// contributes ~3e-6 relative, inside the 1e-5 bar at any K).
+#ifndef FB_BF16_KP
+#define FB_BF16_KP 16
+#endif
+constexpr int KP_BLOCKS = FB_BF16_KP;
 constexpr int GROUP_M = FB_BF16_GROUP_M;
 
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {

@@ -204,7 +204,7 @@ def test_gemm_path_variants(fb, knobs, dt, monkeypatch):
                                       (2048, 2048, 2048, False), (40, 24, 8, True)])
 def test_gemm_bf16_vs_oracle(fb, m, n, k, bt):
     """fb_matmul_bf16: the product of the bf16 inputs (exact in FP64) within 1e-5
-    (FP32 accumulation, RN promotion every 256 k)."""
+    (FP32 accumulation, RN promotion every 1024 k)."""
     A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(torch.bfloat16).cuda()
     Bk = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).to(torch.bfloat16).cuda()
     B = Bk.t().contiguous() if bt else Bk
@@ -212,6 +212,19 @@ def test_gemm_bf16_vs_oracle(fb, m, n, k, bt):
     torch.cuda.synchronize()
     ref = oracle.matmul(A.float().cpu().numpy().astype(np.float64), Bk.float().cpu().numpy().astype(np.float64))
     assert oracle.rel_l2(C.cpu().numpy(), ref) < 1e-5
+
+
+def test_gemm_bf16_k8192_sampled(fb):
+    """Long K (8192 = 8 promotion intervals): sampled full rows against the exact product."""
+    m, n, k = 512, 768, 8192
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(torch.bfloat16).cuda()
+    Bk = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).to(torch.bfloat16).cuda()
+    C = fb.matmul_bf16(A, Bk.t().contiguous(), b_transposed=True)
+    torch.cuda.synchronize()
+    rows = np.array([0, 1, 127, 128, 255, 300, 511])
+    Ad = A.float().cpu().numpy().astype(np.float64)[rows]
+    ref = oracle.matmul(Ad, Bk.float().cpu().numpy().astype(np.float64))
+    assert oracle.rel_l2(C.cpu().numpy()[rows], ref) < 1e-5
 
 
 def test_gemm_bf16_multicast_cluster(fb, monkeypatch):
