@@ -323,17 +323,20 @@ def test_fft_path_variants_vs_oracle(fb, n0, n1, knobs, monkeypatch):
 
 @pytest.mark.parametrize("n0,n1", [(512, 512), (2048, 2048), (8192, 256)])
 def test_store_path_and_stagger_bitwise(fb, n0, n1, monkeypatch):
-    """The column-output path (exchange buffer + TMA store vs direct register stores) and the
-    staggered start change only how bytes move, not the arithmetic: results are bit-identical."""
+    """The column-output path (exchange buffer + TMA store vs direct register stores), the
+    staggered start and the pair step's lane-exchange layout change only how bytes move, not the
+    arithmetic: results are bit-identical (forward and inverse)."""
     xh = synth.complex_field(n0, n1)
     x = torch.from_numpy(xh).cuda()
     outs = []
-    for knobs in ({}, {"FB_FFT_COL_STG": "0"}, {"FB_FFT_COL_STG": "1"}, {"FB_FFT_STAGGER": "0"}):
-        for k in ("FB_FFT_COL_STG", "FB_FFT_STAGGER"):
+    for knobs in ({}, {"FB_FFT_COL_STG": "0"}, {"FB_FFT_COL_STG": "1"}, {"FB_FFT_STAGGER": "0"},
+                  {"FB_FFT_PAIR2": "0"}):
+        for k in ("FB_FFT_COL_STG", "FB_FFT_STAGGER", "FB_FFT_PAIR2"):
             monkeypatch.delenv(k, raising=False)
         for k, v in knobs.items():
             monkeypatch.setenv(k, v)
-        outs.append(fb.fft2d(x).cpu().numpy())
+        y = fb.fft2d(x)
+        outs.append(np.concatenate([y.cpu().numpy(), fb.ifft2d(y).cpu().numpy()]))
     for o in outs[1:]:
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
 

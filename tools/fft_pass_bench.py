@@ -45,4 +45,5 @@ for i in range(reps + 5):
 ts.sort()
 knobs = {k: v for k, v in os.environ.items() if k.startswith("FB_FFT") or k == "FLUSH"}
 print(json.dumps({"n0": n0, "n1": n1, "ms": sum(ts) / len(ts), "ms_min": ts[0], "ms_med": ts[len(ts) // 2],
+                  "ms_p10": ts[len(ts) // 10], "ms_p90": ts[(9 * len(ts)) // 10],
                   "knobs": knobs}))
