@@ -107,6 +107,7 @@ struct FftPass {
     int sm_count;   //   (set by launch_fft_pass)
     int pair_half_shfl; // pair step: 0 lane exchange per element, 1 per element pair, 2 fused into the
                         //   last row stage, no exchange (default; knob FB_FFT_PAIR2)
+    int col_pair_last; // column pass: last stage on column pairs with 16-byte shared accesses (knob)
     int col_stg;    // persistent column pass: 1 outputs by direct stores, 0 X + TMA store, -1 auto
     int pair_log2N; // >0: lines come in pairs (g = 2q + c, rows q and q + N/2 of an N-long column);
                     // after the row FFT, the radix-2 column butterfly across the pair and the

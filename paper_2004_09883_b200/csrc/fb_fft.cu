@@ -30,6 +30,7 @@ fb_status launch_fft_pass(const FftPass& p_in, const DeviceState* st, cudaStream
     p.sm_count = st->sm_count;
     p.col_stg = fft_knob("FB_FFT_COL_STG", -1);
     p.pair_half_shfl = fft_knob("FB_FFT_PAIR2", 2);
+    p.col_pair_last = fft_knob("FB_FFT_COLPAIR", 0);
     switch (p.log2L) {
         case 0: return launch_pass_L<0>(p, st, s);
         case 1: return launch_pass_L<1>(p, st, s);

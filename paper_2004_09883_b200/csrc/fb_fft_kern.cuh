@@ -263,11 +263,12 @@ __device__ __forceinline__ void pair_radix2(float2* v, int c, float2 w) {
 }
 
 // Last row stage of the pair plan fused with the pair step (C = 2 lines q, q + N/2 interleaved in
-// the exchange buffer): thread (c, t) runs butterflies q = c Q/2 ... c Q/2 + Q/2 - 1 of BOTH
+// the exchange buffer): thread (c, t) runs butterflies j = 2t + c + 2T qq (qq < Q/2) of BOTH
 // lines (same butterfly arithmetic and twiddles as Stages), so the radix-2 across the pair is
 // thread-local (no lane exchange) and each twiddle serves two lines; X0 = x0 + x1 goes to row q,
 // X1 = (x0 - x1) W_N^q to row q + N/2 (the formulas of pair_radix2, bitwise).  Interleaved A/B
-// at 2048^2 (4 x 200 reps): 37.80 us (one exchange per element pair) -> 36.97 us.
+// at 2048^2 (4 x 200 reps): 37.80 us (one exchange per element pair) -> 36.97 us (butterfly
+// j = t + cT, 8-byte loads) -> 35.99 us (j = 2t + c, 16-byte loads of both rows' element k).
 template <int LOG2L>
 struct PairLast {
     using G = LineGeom<LOG2L>;
@@ -282,14 +283,17 @@ struct PairLast {
             constexpr int T = G::T, L = G::L, QH = Q / 2;
 #pragma unroll
             for (int qq = 0; qq < QH; ++qq) {
-                const int j = t + (c * QH + qq) * T;
+                // butterfly j = 2t + c + 2T qq: adjacent lanes take adjacent butterflies, so each
+                // 16-byte load (element k of both rows, interleaved in X) and each store is
+                // contiguous across the warp
+                const int j = 2 * t + c + qq * 2 * T;
                 const float2* twp = stw + stage_tw_offset(LOG2L, S) + (j & (Ns - 1));
                 float2 b0[R], b1[R];
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const float2* xp = X + padk(j + r * (L / R)) * 2;
-                    b0[r] = xp[0];
-                    b1[r] = xp[1];
+                    const float4 x01 = *reinterpret_cast<const float4*>(X + padk(j + r * (L / R)) * 2);
+                    b0[r] = make_float2(x01.x, x01.y);
+                    b1[r] = make_float2(x01.z, x01.w);
                 }
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
@@ -304,6 +308,69 @@ struct PairLast {
                     const int k = j + r * (L / R);
                     row0[k] = cadd(b0[r], b1[r]);
                     row1[k] = cmul(csub(b0[r], b1[r]), w);
+                }
+            }
+        }
+    }
+};
+
+// Last stage of a column pass (C interleaved columns, C even) with 16-byte shared accesses:
+// thread (c, t) runs butterflies j = 2t + (c & 1) + 2T qq (qq < Q/2) of the column PAIR
+// (2 (c >> 1), 2 (c >> 1) + 1) -- both columns' element k are adjacent in the exchange buffer and
+// in the dense output staging [k][C], so inputs and outputs move as float4 (half the shared-memory
+// instructions) and each twiddle serves two columns.  Same butterfly arithmetic as Stages, then
+// the conj/scale epilogue; writes the results to X as the TMA store expects (after a barrier:
+// other threads may still be reading their inputs).  Knob FB_FFT_COLPAIR=1; A/B neutral at
+// 2048^2 (35.99 vs 35.99 us) and 4096^2, so it is off by default.
+template <int LOG2L, int C>
+struct ColPairLast {
+    using G = LineGeom<LOG2L>;
+    static constexpr int S = G::NSTAGES - 1;
+    static constexpr int R = stage_radix(LOG2L, S);
+    static constexpr int Ns = 1 << (4 * S);
+    static constexpr int Q = G::E / R;
+    static constexpr bool ok = (G::NSTAGES >= 2) && (Q % 2 == 0) && (C % 2 == 0);
+    __device__ __forceinline__ static void run(float2* X, int t, int c, const float2* __restrict__ stw,
+                                               int conj_out, float scale) {
+        if constexpr (ok) {
+            constexpr int T = G::T, L = G::L, QH = Q / 2;
+            const int cp = c & ~1;  // first column of the pair
+            float2 b0[QH][R], b1[QH][R];
+#pragma unroll
+            for (int qq = 0; qq < QH; ++qq) {
+                const int j = 2 * t + (c & 1) + qq * 2 * T;
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const float4 x01 = *reinterpret_cast<const float4*>(X + padk(j + r * (L / R)) * C + cp);
+                    b0[qq][r] = make_float2(x01.x, x01.y);
+                    b1[qq][r] = make_float2(x01.z, x01.w);
+                }
+            }
+            __syncthreads();  // every thread has read its last-stage inputs; X becomes the output staging
+#pragma unroll
+            for (int qq = 0; qq < QH; ++qq) {
+                const int j = 2 * t + (c & 1) + qq * 2 * T;
+                const float2* twp = stw + stage_tw_offset(LOG2L, S) + (j & (Ns - 1));
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    const float2 wr = __ldg(twp + r * Ns);
+                    b0[qq][r] = cmul(b0[qq][r], wr);
+                    b1[qq][r] = cmul(b1[qq][r], wr);
+                }
+                dft<R>(b0[qq]);
+                dft<R>(b1[qq]);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 y0 = b0[qq][r], y1 = b1[qq][r];
+                    if (conj_out) {
+                        y0.y = -y0.y;
+                        y1.y = -y1.y;
+                    }
+                    if (scale != 1.0f) {
+                        y0 = __fmul2_rn(y0, bc2(scale));
+                        y1 = __fmul2_rn(y1, bc2(scale));
+                    }
+                    *reinterpret_cast<float4*>(X + (j + r * (L / R)) * C + cp) = make_float4(y0.x, y0.y, y1.x, y1.y);
                 }
             }
         }
@@ -678,6 +745,24 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
                 const int64_t gq = (grp * C) >> ((gshift >= 62) ? 62 : gshift);
                 float2* row0 = p.out + gq * p.lout.hi;
                 PairLast<LOG2L>::run(X, t, c, stw, wpair, row0, row0 + p.lout.lo);
+                continue;
+            }
+        }
+        if constexpr (KIND == KIND_COL && ColPairLast<LOG2L, C>::ok) {
+            if (p.col_pair_last && !p.col_stg && p.tw4_log2N == 0 && p.pair_log2N == 0 && !p.debug) {
+                Stages<LOG2L, C, 0, ColPairLast<LOG2L, C>::S>::run(v, X, t, c, stw, nullptr);
+                ColPairLast<LOG2L, C>::run(X, t, c, stw, p.conj_out, p.scale);
+                ptx::fence_proxy_async_smem();
+                __syncthreads();
+                if (tid == 0) {
+                    const int64_t g0 = grp * C;
+                    const int64_t gh0 = (gshift >= 62) ? 0 : (g0 >> gshift);
+                    const int gl0 = (int)(g0 & gmask);
+#pragma unroll 1
+                    for (int kb = 0; kb < L; kb += TG::BOX)
+                        ptx::tma_store_3d(&tout, ptx::smem_u32(X + kb * C), gl0, kb, (int)gh0);
+                    ptx::bulk_commit();
+                }
                 continue;
             }
         }

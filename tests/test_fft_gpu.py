@@ -321,7 +321,8 @@ def test_fft_path_variants_vs_oracle(fb, n0, n1, knobs, monkeypatch):
     assert oracle.rel_l2(z.cpu().numpy(), xh) < 5e-7
 
 
-@pytest.mark.parametrize("n0,n1", [(512, 512), (2048, 2048), (8192, 256), (1024, 1024), (2048, 4096), (512, 64)])
+@pytest.mark.parametrize("n0,n1", [(512, 512), (2048, 2048), (8192, 256), (1024, 1024), (2048, 4096), (512, 64),
+                                   (4096, 4096), (256, 1024), (64, 2048)])
 def test_store_path_and_stagger_bitwise(fb, n0, n1, monkeypatch):
     """The column-output path (exchange buffer + TMA store vs direct register stores), the
     staggered start and the pair step's lane-exchange layout change only how bytes move, not the
@@ -330,8 +331,9 @@ def test_store_path_and_stagger_bitwise(fb, n0, n1, monkeypatch):
     x = torch.from_numpy(xh).cuda()
     outs = []
     for knobs in ({}, {"FB_FFT_COL_STG": "0"}, {"FB_FFT_COL_STG": "1"}, {"FB_FFT_STAGGER": "0"},
-                  {"FB_FFT_PAIR2": "0"}, {"FB_FFT_PAIR2": "1"}, {"FB_FFT_PAIR2": "2"}):
-        for k in ("FB_FFT_COL_STG", "FB_FFT_STAGGER", "FB_FFT_PAIR2"):
+                  {"FB_FFT_PAIR2": "0"}, {"FB_FFT_PAIR2": "1"}, {"FB_FFT_PAIR2": "2"},
+                  {"FB_FFT_COLPAIR": "0"}, {"FB_FFT_COLPAIR": "1"}):
+        for k in ("FB_FFT_COL_STG", "FB_FFT_STAGGER", "FB_FFT_PAIR2", "FB_FFT_COLPAIR"):
             monkeypatch.delenv(k, raising=False)
         for k, v in knobs.items():
             monkeypatch.setenv(k, v)
