@@ -302,6 +302,92 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// split_both_kernel with 4x the work per thread (all loads of a thread issued before its first
+// store): blocks [0, nblk_a) take 1024 consecutive float4 chunks of A's rows (flattened over
+// rows, so short rows do not leave threads idle; m * ceil(k/4) < 2^31 is checked by the
+// caller), the rest split-transpose 64 x 64 tiles of B through padded shared memory
+// (conflict-free: pitch 65).  Same split1 per element, so the outputs are bitwise identical.
+__global__ void __launch_bounds__(256)
+    split_both_wide_kernel(const float* __restrict__ A, int64_t m, int64_t k, int64_t lda, float* __restrict__ Ah,
+                           float* __restrict__ Al, const float* __restrict__ B, int64_t n, int64_t ldb,
+                           float* __restrict__ Bh, float* __restrict__ Bl, int64_t ldo, int64_t nblk_a) {
+    __shared__ float th[64][65], tl[64][65];
+    const int64_t bid = blockIdx.x;
+    const int tid = threadIdx.x;
+    if (bid < nblk_a) {
+        const uint32_t ck = (uint32_t)((k + 3) / 4);
+        const uint32_t total = (uint32_t)m * ck;
+        float4 x[4];
+        uint32_t rr[4], cc[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t q = (uint32_t)bid * 1024u + (uint32_t)u * 256u + (uint32_t)tid;
+            rr[u] = q / ck;
+            cc[u] = (q - rr[u] * ck) * 4u;
+            if (q < total && cc[u] + 4 <= k) x[u] = *reinterpret_cast<const float4*>(A + rr[u] * lda + cc[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint32_t q = (uint32_t)bid * 1024u + (uint32_t)u * 256u + (uint32_t)tid;
+            if (q >= total) continue;
+            const float* xr = A + (int64_t)rr[u] * lda;
+            float* hr = Ah + (int64_t)rr[u] * ldo;
+            float* lr = Al + (int64_t)rr[u] * ldo;
+            const int64_t c4 = cc[u];
+            if (c4 + 4 <= k) {
+                float4 h, l;
+                split1(x[u].x, h.x, l.x);
+                split1(x[u].y, h.y, l.y);
+                split1(x[u].z, h.z, l.z);
+                split1(x[u].w, h.w, l.w);
+                *reinterpret_cast<float4*>(hr + c4) = h;
+                *reinterpret_cast<float4*>(lr + c4) = l;
+            } else {
+                for (int64_t c = c4; c < k; ++c) split1(xr[c], hr[c], lr[c]);
+            }
+        }
+        return;
+    }
+    // B [k][n] -> hi/lo [n][ldo], 64 x 64 tiles
+    const int64_t tb = bid - nblk_a;
+    const int64_t tiles_c = (n + 63) / 64;
+    const int64_t r0 = (tb / tiles_c) * 64, c0 = (tb % tiles_c) * 64;
+    const int lane = tid & 31, w = tid >> 5;  // 8 warps
+    float xv[16];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t r = r0 + w + 8 * j, c = c0 + lane + 32 * h;
+            xv[2 * j + h] = (r < k && c < n) ? B[r * ldb + c] : 0.f;
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            float hf, lf;
+            split1(xv[2 * j + h], hf, lf);
+            th[w + 8 * j][lane + 32 * h] = hf;
+            tl[w + 8 * j][lane + 32 * h] = lf;
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const int64_t c = c0 + w + 8 * j;  // output row (= column of B)
+        if (c >= n) continue;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t r = r0 + lane + 32 * h;
+            if (r < k) {
+                Bh[c * ldo + r] = th[lane + 32 * h][w + 8 * j];
+                Bl[c * ldo + r] = tl[lane + 32 * h][w + 8 * j];
+            }
+        }
+    }
+}
+
 __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, int& tm, int& tn) {
     const int per_group = GROUP_M * tiles_n;
     const int grp = tile / per_group;
@@ -750,6 +836,18 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
     if (sk && sk[0] == '1') {
         FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
         FB_TRY(tf32_split_device(1, k, n, (const float*)B, ldb, Bh, Bl, kp, st, s));
+    } else if (!(getenv("FB_GEMM_SPLITV") && getenv("FB_GEMM_SPLITV")[0] == '1') &&
+               m * ((k + 3) / 4) + 1024 < INT32_MAX) {
+        // default: the wide split (A/B knob FB_GEMM_SPLITV=1: split_both_kernel)
+        const int64_t nblk_a = (m * ((k + 3) / 4) + 1023) / 1024;
+        const int64_t nblk_b = ((k + 63) / 64) * ((n + 63) / 64);
+        if (nblk_a + nblk_b > INT32_MAX) {
+            set_error("split grid too large");
+            return FB_ERR_UNSUPPORTED_SIZE;
+        }
+        tf32::split_both_wide_kernel<<<(unsigned)(nblk_a + nblk_b), 256, 0, s>>>(
+            (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a);
+        FB_LAUNCH_CHECK("split_both_wide_kernel");
     } else {
         const int a_cblk = (int)((((k + 3) / 4) + 255) / 256);
         const int64_t nblk_a = m * a_cblk;

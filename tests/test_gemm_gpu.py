@@ -63,6 +63,25 @@ def test_f32_padded_leading_dims(fb):
     assert torch.all(Cb[:, n:] == 0)
 
 
+@pytest.mark.parametrize("m,n,k", [(200, 100, 150), (300, 260, 203), (2048, 2048, 2048), (64, 1000, 8)])
+def test_f32_wide_split_bitwise(fb, m, n, k, monkeypatch):
+    """The default operand split (split_both_wide_kernel: flattened float4 chunks of A, 64 x 64
+    tiles of B, ragged k and n) gives C bit for bit equal to the 32 x 32-tile split_both_kernel
+    (knob FB_GEMM_SPLITV=1): same split per element, same GEMM."""
+    Ab = torch.from_numpy(synth.real_matrix(m, (k + 3) // 4 * 4, synth.TID_GEMM_A)).cuda()
+    Bb = torch.from_numpy(synth.real_matrix(k, (n + 3) // 4 * 4, synth.TID_GEMM_B)).cuda()
+    A, B = Ab[:, :k], Bb[:, :n]
+    C1 = fb.matmul(A, B)
+    torch.cuda.synchronize()
+    monkeypatch.setenv("FB_GEMM_SPLITV", "1")
+    C0 = fb.matmul(A, B)
+    torch.cuda.synchronize()
+    assert torch.equal(C0, C1)
+    if m * n * k <= 2 ** 24:
+        ref = oracle.matmul(A.cpu().numpy().copy(), B.cpu().numpy().copy())
+        assert oracle.rel_l2(C1.cpu().numpy(), ref) < 1e-5
+
+
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
 def test_2048_config2_full_oracle(fb, dt):
     """BASELINE configs[2]: 2048^3 in FP64 and FP32, full oracle."""
@@ -185,6 +204,7 @@ def test_gemm_ex_beta0_ignores_nan_and_alpha0(fb):
 
 
 @pytest.mark.parametrize("knobs,dt", [({"FB_GEMM_1CTA": "1"}, torch.float32), ({"FB_GEMM_SPLIT2": "1"}, torch.float32),
+                                      ({"FB_GEMM_SPLITV": "1"}, torch.float32),
                                       ({"FB_F64_CFG": "1"}, torch.float64), ({"FB_F64_CFG": "2"}, torch.float64)])
 def test_gemm_path_variants(fb, knobs, dt, monkeypatch):
     """The kernels behind A/B knobs (1-CTA tcgen05 kernel, two split launches, the larger FP64
