@@ -26,7 +26,7 @@ fb_status launch_fft_pass(const FftPass& p_in, const DeviceState* st, cudaStream
     if (p_in.nlines <= 0) return FB_OK;
     FftPass p = p_in;
     p.debug = fft_knob("FB_FFT_DEBUG", 0);
-    p.stagger_ns = fft_knob("FB_FFT_STAGGER", 300);
+    p.stagger_ns = fft_knob("FB_FFT_STAGGER", 600);
     p.sm_count = st->sm_count;
     p.col_stg = fft_knob("FB_FFT_COL_STG", -1);
     p.pair_half_shfl = fft_knob("FB_FFT_PAIR2", 2);

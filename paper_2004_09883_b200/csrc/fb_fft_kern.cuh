@@ -690,7 +690,9 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
         // Staggered start: CTA slot s (the s-th CTA placed on an SM) issues its first load
         // s * stagger_ns later, so the slot-0 CTAs get their first group from a less crowded
         // memory system and start computing earlier (interleaved A/B at 2048^2, 4 x 150 reps:
-        // 38.74 -> 38.21 us at 300 ns; no effect at 1024^2 / 4096^2).  Knob FB_FFT_STAGGER (ns).
+        // 38.74 -> 38.21 us at 300 ns; no effect at 1024^2 / 4096^2).  Knob FB_FFT_STAGGER (ns);
+        // default 600 since the fused pair stage (3 x 200 reps interleaved, 2048^2: 300 ns 36.20,
+        // 600 ns 35.87, 900 ns 35.86, 1200 ns 35.95 us; 1024^2 / 4096^2 within 0.05 us).
         if (p.stagger_ns > 0 && p.sm_count > 0) {
             const int slot = (int)(blockIdx.x / (unsigned)p.sm_count);
             for (int i = 0; i < slot; ++i) __nanosleep((unsigned)p.stagger_ns);
