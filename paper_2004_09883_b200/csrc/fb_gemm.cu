@@ -310,10 +310,14 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     split_both_wide_kernel(const float* __restrict__ A, int64_t m, int64_t k, int64_t lda, float* __restrict__ Ah,
                            float* __restrict__ Al, const float* __restrict__ B, int64_t n, int64_t ldb,
-                           float* __restrict__ Bh, float* __restrict__ Bl, int64_t ldo, int64_t nblk_a) {
+                           float* __restrict__ Bh, float* __restrict__ Bl, int64_t ldo, int64_t nblk_a,
+                           int pdl_trigger) {
     __shared__ float th[64][65], tl[64][65];
     const int64_t bid = blockIdx.x;
     const int tid = threadIdx.x;
+    // let the GEMM grid (launched with programmatic serialization) be scheduled as SMs free up;
+    // its griddepcontrol.wait still waits for this whole grid and its memory (knob FB_GEMM_SPLIT_PDL)
+    if (pdl_trigger) ptx::pdl_launch_dependents();
     if (bid < nblk_a) {
         const uint32_t ck = (uint32_t)((k + 3) / 4);
         const uint32_t total = (uint32_t)m * ck;
@@ -846,7 +850,8 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
             return FB_ERR_UNSUPPORTED_SIZE;
         }
         tf32::split_both_wide_kernel<<<(unsigned)(nblk_a + nblk_b), 256, 0, s>>>(
-            (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a);
+            (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a,
+            (getenv("FB_GEMM_SPLIT_PDL") && getenv("FB_GEMM_SPLIT_PDL")[0] == '1') ? 1 : 0);
         FB_LAUNCH_CHECK("split_both_wide_kernel");
     } else {
         const int a_cblk = (int)((((k + 3) / 4) + 255) / 256);
