@@ -27,6 +27,9 @@ KEYS = [
     ("sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_pct"),
     ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed", "tensor_pipe_pct"),
     ("sm__inst_executed_pipe_tc.avg.pct_of_peak_sustained_active", "tc_inst_pct"),
+    # tcgen05 (UMMA) tensor-core activity; the *_realtime "tensor_pipe" counter above does not
+    # track tcgen05.mma on sm_100
+    ("sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active", "umma_active_pct"),
     ("sm__inst_executed_pipe_tensor_subpipe_dmma.avg.pct_of_peak_sustained_active", "dmma_inst_pct"),
     ("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active", "fp64_pipe_pct"),
     ("l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "smem_bank_conflicts"),
