@@ -153,21 +153,59 @@ __host__ __device__ constexpr int64_t stage_tw_offset(int l, int s) {
     return off;
 }
 
-// Twiddles of stage S for this thread's butterflies j = t + q T: tw[q][r-1] = W_{Ns R}^{(j mod Ns) r}.
+// Twiddles of stage S for this thread's butterflies j = t + q T: W_{Ns R}^{(j mod Ns) r}, r < R.
+// FB_FFT_TWREC = 1 (default): only the log2(R) "bases" W^{jm 2^i} are loaded per butterfly
+// (tw[q][i]); tw_expand forms the other R - 1 - log2(R) powers by products of at most
+// popcount(r) - 1 complex multiplies (<= 3 for R = 16), so each radix-16 stage issues 4
+// table loads per butterfly instead of 15 (the loads were the largest stall of both 2048^2
+// passes: long scoreboard 22 % / 28 % of warp samples, profiles/r1_fft2048_full.txt).
+// FB_FFT_TWREC = 0: all R - 1 twiddles are loaded (tw[q][r-1]), each RN of the FP64 value.
+#ifndef FB_FFT_TWREC
+#define FB_FFT_TWREC 1
+#endif
+__host__ __device__ constexpr int ilog2c(int r) { return r <= 1 ? 0 : 1 + ilog2c(r / 2); }  // floor(log2 r)
+template <int R>
+struct TwCount {
+    static constexpr int value = FB_FFT_TWREC ? ilog2c(R) : R - 1;
+};
+// full[r - 1] = W^{jm r} for r = 1 .. R-1 from the loaded values `b` (bases or, without
+// FB_FFT_TWREC, all of them).  r = hb + rest (hb = highest power of two <= r):
+// W^{jm r} = W^{jm rest} * W^{jm hb}.
+template <int R, int r = 1>
+__device__ __forceinline__ void tw_expand(float2* full, const float2* b) {
+    if constexpr (r < R) {
+        if constexpr (FB_FFT_TWREC) {
+            constexpr int i = ilog2c(r), hb = 1 << i;
+            if constexpr (r == hb)
+                full[r - 1] = b[i];
+            else
+                full[r - 1] = cmul(full[r - hb - 1], b[i]);
+        } else {
+            full[r - 1] = b[r - 1];
+        }
+        tw_expand<R, r + 1>(full, b);
+    }
+}
+// load this butterfly's stored twiddles from the [r][jm] table row base twp (= table + jm)
+template <int R, int Ns>
+__device__ __forceinline__ void tw_load(float2* b, const float2* __restrict__ twp) {
+#pragma unroll
+    for (int i = 0; i < TwCount<R>::value; ++i) b[i] = __ldg(twp + (FB_FFT_TWREC ? (1 << i) : (i + 1)) * Ns);
+}
+
 template <int LOG2L, int S>
 struct StageTw {
     static constexpr int R = stage_radix(LOG2L, S);
     static constexpr int Q = LineGeom<LOG2L>::E / R;
-    static constexpr int NT = (S == 0) ? 1 : Q * (R - 1);
+    static constexpr int NB = TwCount<R>::value;  // stored twiddles per butterfly
+    static constexpr int NT = (S == 0) ? 1 : Q * NB;
     __device__ __forceinline__ static void load(float2* tw, int t, const float2* __restrict__ stw) {
         if constexpr (S > 0) {
             constexpr int Ns = 1 << (4 * S);
 #pragma unroll
             for (int q = 0; q < Q; ++q) {
                 const int jm = (t + q * LineGeom<LOG2L>::T) & (Ns - 1);
-                const float2* twp = stw + stage_tw_offset(LOG2L, S) + jm;
-#pragma unroll
-                for (int r = 1; r < R; ++r) tw[q * (R - 1) + r - 1] = __ldg(twp + r * Ns);
+                tw_load<R, Ns>(tw + q * NB, stw + stage_tw_offset(LOG2L, S) + jm);
             }
         }
     }
@@ -209,8 +247,10 @@ struct Stages {
 #pragma unroll
                 for (int r = 0; r < R; ++r) b[r] = v[q + r * Q];
                 if constexpr (!first) {
+                    float2 full[R - 1];
+                    tw_expand<R>(full, tw + q * StageTw<LOG2L, S>::NB);
 #pragma unroll
-                    for (int r = 1; r < R; ++r) b[r] = cmul(b[r], tw[q * (R - 1) + r - 1]);
+                    for (int r = 1; r < R; ++r) b[r] = cmul(b[r], full[r - 1]);
                 }
                 dft<R>(b);
 #pragma unroll
@@ -295,11 +335,13 @@ struct PairLast {
                     b0[r] = make_float2(x01.x, x01.y);
                     b1[r] = make_float2(x01.z, x01.w);
                 }
+                float2 tb[TwCount<R>::value], full[R - 1];
+                tw_load<R, Ns>(tb, twp);
+                tw_expand<R>(full, tb);
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    const float2 wr = __ldg(twp + r * Ns);
-                    b0[r] = cmul(b0[r], wr);
-                    b1[r] = cmul(b1[r], wr);
+                    b0[r] = cmul(b0[r], full[r - 1]);
+                    b1[r] = cmul(b1[r], full[r - 1]);
                 }
                 dft<R>(b0);
                 dft<R>(b1);
@@ -351,11 +393,13 @@ struct ColPairLast {
             for (int qq = 0; qq < QH; ++qq) {
                 const int j = 2 * t + (c & 1) + qq * 2 * T;
                 const float2* twp = stw + stage_tw_offset(LOG2L, S) + (j & (Ns - 1));
+                float2 tb[TwCount<R>::value], full[R - 1];
+                tw_load<R, Ns>(tb, twp);
+                tw_expand<R>(full, tb);
 #pragma unroll
                 for (int r = 1; r < R; ++r) {
-                    const float2 wr = __ldg(twp + r * Ns);
-                    b0[qq][r] = cmul(b0[qq][r], wr);
-                    b1[qq][r] = cmul(b1[qq][r], wr);
+                    b0[qq][r] = cmul(b0[qq][r], full[r - 1]);
+                    b1[qq][r] = cmul(b1[qq][r], full[r - 1]);
                 }
                 dft<R>(b0[qq]);
                 dft<R>(b1[qq]);

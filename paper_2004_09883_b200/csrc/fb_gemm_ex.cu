@@ -44,6 +44,12 @@ __global__ void __launch_bounds__(256) axpby_kernel(const T* __restrict__ P, int
 }
 
 static size_t align256(size_t b) { return (b + 255) & ~size_t(255); }
+// leading dimension (elements) of a workspace temporary: rows padded to 16 bytes, the row
+// alignment the fb_matmul kernels assume (float4 / TMA rows)
+static int64_t ld16(int64_t x, size_t es) {
+    const int64_t q = (int64_t)(16 / es);
+    return (x + q - 1) / q * q;
+}
 
 struct GemmExLayout {
     size_t core, opa, opb, t, total;
@@ -52,9 +58,9 @@ static GemmExLayout gemm_ex_layout(int dtype, int ta, int tb, int64_t m, int64_t
     const size_t es = dtype == FB_F32 ? 4 : 8;
     GemmExLayout L;
     L.core = align256(gemm_ws_bytes(dtype, m, n, k));
-    L.opa = ta ? align256((size_t)m * (size_t)(k + (k & 1)) * es) : 0;  // even ld: 16-byte rows
-    L.opb = tb ? align256((size_t)k * (size_t)(n + (n & 1)) * es) : 0;
-    L.t = align256((size_t)m * (size_t)(n + (n & 1)) * es);
+    L.opa = ta ? align256((size_t)m * (size_t)ld16(k, es) * es) : 0;
+    L.opb = tb ? align256((size_t)k * (size_t)ld16(n, es) * es) : 0;
+    L.t = align256((size_t)m * (size_t)ld16(n, es) * es);
     L.total = L.core + L.opa + L.opb + L.t;
     return L;
 }
@@ -84,13 +90,13 @@ static fb_status gemm_ex_typed(int dtype, int ta, int tb, int64_t m, int64_t n, 
     if (alpha != 0.0) {
         if (ta) {  // A stored k x m -> op(A) m x k
             T* at = (T*)(w + L.core);
-            la = k + (k & 1);
+            la = ld16(k, sizeof(T));
             FB_TRY(launch_transpose<T>(a, k, m, lda, at, la, s));
             a = at;
         }
         if (tb) {  // B stored n x k -> op(B) k x n
             T* bt = (T*)(w + L.core + L.opa);
-            lb = n + (n & 1);
+            lb = ld16(n, sizeof(T));
             FB_TRY(launch_transpose<T>(b, n, k, ldb, bt, lb, s));
             b = bt;
         }
@@ -98,7 +104,7 @@ static fb_status gemm_ex_typed(int dtype, int ta, int tb, int64_t m, int64_t n, 
     const bool plain = alpha == 1.0 && beta == 0.0;
     if (plain) return gemm_device(dtype, m, n, k, a, la, b, lb, C, ldc, ws, L.core, st, s);
     T* t = (T*)(w + L.core + L.opa + L.opb);
-    const int64_t lt = n + (n & 1);
+    const int64_t lt = ld16(n, sizeof(T));
     if (alpha != 0.0) FB_TRY(gemm_device(dtype, m, n, k, a, la, b, lb, t, lt, ws, L.core, st, s));
     const int64_t total = m * n;
     int64_t blocks = (total + 255) / 256;
