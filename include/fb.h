@@ -60,6 +60,10 @@ const char* fb_last_error_detail(void);
 /* Number of kernels libfb has launched in this process (all devices).  Lets a harness
  * count the library's own launches inside a timed region. */
 uint64_t fb_launch_count(void);
+/* Re-read the FB_* A/B tuning knobs from the environment (normally read once per process, on
+ * first use; no launch path calls getenv).  For tests and tuning tools that change the
+ * environment inside one process.  Not thread-safe against concurrent launches. */
+void fb_reload_knobs(void);
 
 /* Once per device: checks sm_100, builds the twiddle table W[j] = exp(-2 pi i j/16384)
  * (computed in FP64 with sincospi, RN-rounded to FP32; exact at multiples of pi/2),

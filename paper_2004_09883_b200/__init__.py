@@ -26,7 +26,7 @@ _STATUS = {0: "FB_OK", 1: "FB_ERR_INVALID_VALUE", 2: "FB_ERR_UNSUPPORTED_SIZE", 
 
 # every symbol include/fb.h declares (checked by tests/test_abi.py)
 EXPORTS = [
-    "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_init",
+    "fb_version", "fb_status_string", "fb_last_error_detail", "fb_launch_count", "fb_reload_knobs", "fb_init",
     "fb_fft2d_workspace_bytes", "fb_fft2d", "fb_ifft2d", "fb_fft1d_batched", "fb_ifft1d_batched",
     "fb_gemm_workspace_bytes", "fb_gemm", "fb_rfft2d_workspace_bytes", "fb_rfft2d", "fb_irfft2d",
     "fb_matmul_bf16_workspace_bytes", "fb_matmul_bf16",
@@ -64,6 +64,7 @@ def lib() -> ctypes.CDLL:
         "fb_status_string": ([ci], ctypes.c_char_p),
         "fb_last_error_detail": ([], ctypes.c_char_p),
         "fb_launch_count": ([], u64),
+        "fb_reload_knobs": ([], None),
         "fb_init": ([ci], ci),
         "fb_fft2d_workspace_bytes": ([i64, i64], sz),
         "fb_fft2d": ([vp, vp, i64, i64, vp, sz, vp], ci),
@@ -134,23 +135,20 @@ def launch_count() -> int:
     return int(lib().fb_launch_count())
 
 
+def fb_reload_knobs():
+    """Re-read the FB_* A/B knobs from the environment (libfb reads them once per process)."""
+    lib().fb_reload_knobs()
+
+
 def fb_init(device: int = 0):
     _check("fb_init", lib().fb_init(device))
 
 
 # ------------------------------------------------------------------ workspace cache (plumbing)
-_ws_cache: dict = {}
 
 
-def _workspace(nbytes: int, device) -> torch.Tensor | None:
-    if nbytes == 0:
-        return None
-    key = (torch.device(device).index, "ws")
-    t = _ws_cache.get(key)
-    if t is None or t.numel() < nbytes:
-        t = torch.empty(nbytes, dtype=torch.uint8, device=device)
-        _ws_cache[key] = t
-    return t
+def _workspace(nbytes: int, device, stream=None) -> torch.Tensor | None:
+    return None if nbytes == 0 else _workspace_named(nbytes, device, "ws", stream)
 
 
 # ------------------------------------------------------------------ Fourier block
@@ -177,7 +175,7 @@ def fft2d(x: torch.Tensor, out: torch.Tensor | None = None, inverse: bool = Fals
     out = torch.empty_like(x) if out is None else out
     _fft_check(out)
     n0, n1 = x.shape
-    ws = _workspace(lib().fb_fft2d_workspace_bytes(n0, n1), x.device)
+    ws = _workspace(lib().fb_fft2d_workspace_bytes(n0, n1), x.device, stream)
     (fb_ifft2d if inverse else fb_fft2d)(x, out, ws, stream)
     return out
 
@@ -199,7 +197,7 @@ def rfft2d(x: torch.Tensor, stream=None) -> torch.Tensor:
         raise ValueError("expected a contiguous 2D float32 CUDA tensor")
     n0, n1 = x.shape
     y = torch.empty(n0, n1 // 2 + 1, dtype=torch.complex64, device=x.device)
-    ws = _workspace_named(lib().fb_rfft2d_workspace_bytes(n0, n1), x.device, "rfft")
+    ws = _workspace_named(lib().fb_rfft2d_workspace_bytes(n0, n1), x.device, "rfft", stream)
     _check("fb_rfft2d", lib().fb_rfft2d(_ptr(x), _ptr(y), n0, n1, _ptr(ws), ws.numel(), _stream(stream)))
     return y
 
@@ -210,7 +208,7 @@ def irfft2d(y: torch.Tensor, n1: int, stream=None) -> torch.Tensor:
         raise ValueError("expected a contiguous 2D complex64 CUDA tensor")
     n0 = y.shape[0]
     x = torch.empty(n0, n1, dtype=torch.float32, device=y.device)
-    ws = _workspace_named(lib().fb_rfft2d_workspace_bytes(n0, n1), y.device, "rfft")
+    ws = _workspace_named(lib().fb_rfft2d_workspace_bytes(n0, n1), y.device, "rfft", stream)
     _check("fb_irfft2d", lib().fb_irfft2d(_ptr(y), _ptr(x), n0, n1, _ptr(ws), ws.numel(), _stream(stream)))
     return x
 
@@ -228,7 +226,7 @@ def matmul_bf16(A: torch.Tensor, B: torch.Tensor, b_transposed: bool = False, ou
     m, k = A.shape
     n = B.shape[0] if b_transposed else B.shape[1]
     C = torch.empty(m, n, dtype=torch.float32, device=A.device) if out is None else out
-    ws = _workspace_named(lib().fb_matmul_bf16_workspace_bytes(int(b_transposed), m, n, k), A.device, "bf16")
+    ws = _workspace_named(lib().fb_matmul_bf16_workspace_bytes(int(b_transposed), m, n, k), A.device, "bf16", stream)
     _check("fb_matmul_bf16", lib().fb_matmul_bf16(m, n, k, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
                                                   int(b_transposed), _ptr(C), C.stride(0), _ptr(ws), ws.numel(),
                                                   _stream(stream)))
@@ -244,7 +242,7 @@ def gemm(A: torch.Tensor, B: torch.Tensor, C: torch.Tensor | None = None, alpha:
     n = B.shape[0] if trans_b else B.shape[1]
     if C is None:
         C = torch.zeros(m, n, dtype=A.dtype, device=A.device)
-    ws = _workspace_named(lib().fb_gemm_workspace_bytes(dt, int(trans_a), int(trans_b), m, n, k), A.device, "gemm")
+    ws = _workspace_named(lib().fb_gemm_workspace_bytes(dt, int(trans_a), int(trans_b), m, n, k), A.device, "gemm", stream)
     _check("fb_gemm", lib().fb_gemm(dt, int(trans_a), int(trans_b), m, n, k, float(alpha), _ptr(A), A.stride(0),
                                     _ptr(B), B.stride(0), float(beta), _ptr(C), C.stride(0), _ptr(ws), ws.numel(),
                                     _stream(stream)))
@@ -279,7 +277,7 @@ def matmul(A: torch.Tensor, B: torch.Tensor, out: torch.Tensor | None = None, st
     m, k = A.shape
     n = B.shape[1]
     out = torch.empty((m, n), dtype=A.dtype, device=A.device) if out is None else out
-    ws = _workspace(matmul_workspace_bytes(_dt(A), m, n, k), A.device)
+    ws = _workspace(matmul_workspace_bytes(_dt(A), m, n, k), A.device, stream)
     fb_matmul(A, B, out, ws, stream)
     return out
 
@@ -300,18 +298,20 @@ def fb_matmul_3xtf32_presplit(Ah, Al, Bh, Bl, C, stream=None):
 
 
 # ------------------------------------------------------------------ host interface
-def _host_buf(n_bytes: int, device):
-    return _workspace_named(n_bytes, device, "host_dev")
-
-
 _named: dict = {}
 
 
-def _workspace_named(nbytes, device, name):
-    key = (torch.device(device).index, name)
+def _workspace_named(nbytes, device, name, stream=None):
+    """Scratch buffer cached per (device, name, stream): calls on different streams never share
+    one.  Growing it synchronises the device first, so no kernel queued on that stream still
+    uses the old buffer when it goes back to torch's caching allocator."""
+    dev = torch.device(device)
+    key = (dev.index, name, _stream(stream))
     t = _named.get(key)
     if t is None or t.numel() < nbytes:
-        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=device)
+        if t is not None:
+            torch.cuda.synchronize(dev)
+        t = torch.empty(max(nbytes, 1), dtype=torch.uint8, device=dev)
         _named[key] = t
     return t
 
@@ -320,7 +320,7 @@ def fb_fft2d_host(x_host: torch.Tensor, y_host: torch.Tensor, inverse: bool = Fa
     """HOST complex64 in -> H2D -> 2D FFT -> D2H -> HOST out (synchronous)."""
     n0, n1 = x_host.shape
     need = lib().fb_fft2d_host_workspace_bytes(n0, n1)
-    dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
+    dev = _workspace_named(need, torch.device("cuda", device), "host_dev", stream)
     _check("fb_fft2d_host", lib().fb_fft2d_host(_ptr(x_host), _ptr(y_host), n0, n1, int(inverse), _ptr(dev),
                                                 dev.numel(), _stream(stream)))
 
@@ -330,7 +330,7 @@ def fb_fft2d_host_batch(x_host: torch.Tensor, y_host: torch.Tensor, inverse: boo
     (copies of consecutive transforms overlap in both PCIe directions) -> HOST out (synchronous)."""
     b, n0, n1 = x_host.shape
     need = lib().fb_fft2d_host_batch_workspace_bytes(n0, n1)
-    dev = _workspace_named(need, torch.device("cuda", device), "host_batch_dev")
+    dev = _workspace_named(need, torch.device("cuda", device), "host_batch_dev", stream)
     _check("fb_fft2d_host_batch", lib().fb_fft2d_host_batch(_ptr(x_host), _ptr(y_host), n0, n1, b, int(inverse),
                                                             _ptr(dev), dev.numel(), _stream(stream)))
 
@@ -340,7 +340,7 @@ def fb_matmul_host(A_host: torch.Tensor, B_host: torch.Tensor, C_host: torch.Ten
     n = B_host.shape[1]
     dt = _dt(A_host)
     need = lib().fb_matmul_host_workspace_bytes(dt, m, n, k)
-    dev = _workspace_named(need, torch.device("cuda", device), "host_dev")
+    dev = _workspace_named(need, torch.device("cuda", device), "host_dev", stream)
     _check("fb_matmul_host", lib().fb_matmul_host(dt, m, n, k, _ptr(A_host), _ptr(B_host), _ptr(C_host),
                                                   _ptr(dev), dev.numel(), _stream(stream)))
 
@@ -417,7 +417,7 @@ def fb_fft2d_slab_model(P: int, x, y, n0: int, n1: int, inverse: bool = False, s
     """Single-GPU model of the fused slab path for P virtual ranks (fb.h): forward x (n0 x n1)
     -> y = the P column slabs [P][n0][n1/P]; inverse y -> x."""
     win = torch.empty(n0 * n1, dtype=torch.complex64, device=x.device)
-    ws = _workspace_named(lib().fb_fft2d_slab_workspace_bytes(P, n0, n1), x.device, "slab_model")
+    ws = _workspace_named(lib().fb_fft2d_slab_workspace_bytes(P, n0, n1), x.device, "slab_model", stream)
     _check("fb_fft2d_slab_model", lib().fb_fft2d_slab_model(P, int(inverse), _ptr(x), _ptr(y), n0, n1, _ptr(win),
                                                             _ptr(ws), ws.numel(), _stream(stream)))
 
@@ -448,13 +448,13 @@ class Comm:
 
     def fb_fft2d_slab(self, x_rows, y_cols, n0, n1, ws=None, stream=None):
         need = lib().fb_fft2d_slab_workspace_bytes(self.world, n0, n1)
-        ws = _workspace_named(need, x_rows.device, "slab") if ws is None else ws
+        ws = _workspace_named(need, x_rows.device, "slab", stream) if ws is None else ws
         _check("fb_fft2d_slab", lib().fb_fft2d_slab(self.handle, _ptr(x_rows), _ptr(y_cols), n0, n1, _ptr(ws),
                                                     ws.numel(), _stream(stream)))
 
     def fb_ifft2d_slab(self, y_cols, x_rows, n0, n1, ws=None, stream=None):
         need = lib().fb_fft2d_slab_workspace_bytes(self.world, n0, n1)
-        ws = _workspace_named(need, y_cols.device, "slab") if ws is None else ws
+        ws = _workspace_named(need, y_cols.device, "slab", stream) if ws is None else ws
         _check("fb_ifft2d_slab", lib().fb_ifft2d_slab(self.handle, _ptr(y_cols), _ptr(x_rows), n0, n1, _ptr(ws),
                                                       ws.numel(), _stream(stream)))
 
@@ -464,7 +464,7 @@ class Comm:
         m = mp * self.world
         dt = _dt(A_rows)
         need = lib().fb_matmul_rowblock_workspace_bytes(self.world, dt, m, n, k)
-        ws = _workspace_named(need, A_rows.device, "rowblock") if ws is None else ws
+        ws = _workspace_named(need, A_rows.device, "rowblock", stream) if ws is None else ws
         _check("fb_matmul_rowblock", lib().fb_matmul_rowblock(
             self.handle, dt, m, n, k, _ptr(A_rows), A_rows.stride(0), _ptr(B), B.stride(0), root, _ptr(C_rows),
             C_rows.stride(0), _ptr(ws), ws.numel(), _stream(stream)))

@@ -19,6 +19,66 @@ void set_error(const char* fmt, ...) {
 }
 void clear_error() { t_err[0] = 0; }
 
+// ---------------------------------------------------------------- knobs (fb_common.cuh)
+static int env_int(const char* name, int dflt) {
+    const char* e = getenv(name);
+    return (e && e[0]) ? atoi(e) : dflt;
+}
+static Knobs read_knobs() {
+    Knobs k;
+    k.fft_stagger_ns = env_int("FB_FFT_STAGGER", k.fft_stagger_ns);
+    k.fft_col_stg = env_int("FB_FFT_COL_STG", k.fft_col_stg);
+    k.fft_pair2 = env_int("FB_FFT_PAIR2", k.fft_pair2);
+    k.fft_colpair = env_int("FB_FFT_COLPAIR", k.fft_colpair);
+    k.fft_col_max_log2 = env_int("FB_FFT_COL_MAX_LOG2", k.fft_col_max_log2);
+    k.fft_4step_lb = env_int("FB_FFT_4STEP_LB", k.fft_4step_lb);
+    k.fft_pair = env_int("FB_FFT_PAIR", k.fft_pair);
+    k.fft_pair_max_log2 = env_int("FB_FFT_PAIR_MAX_LOG2", k.fft_pair_max_log2);
+    k.fft_no_tma_col = env_int("FB_FFT_NO_TMA_COL", k.fft_no_tma_col);
+    k.fft_col_c = env_int("FB_FFT_COL_C", k.fft_col_c);
+    k.fft_no_tma_row = env_int("FB_FFT_NO_TMA_ROW", k.fft_no_tma_row);
+    k.fft_col_nb = env_int("FB_FFT_COL_NB", k.fft_col_nb);
+    k.fft_row_nb = env_int("FB_FFT_ROW_NB", k.fft_row_nb);
+    k.fft_no_tma = env_int("FB_FFT_NO_TMA", k.fft_no_tma);
+    k.fft_longrow = env_int("FB_FFT_LONGROW", k.fft_longrow);
+    k.fft_pair_tma = env_int("FB_FFT_PAIR_TMA", k.fft_pair_tma);
+    k.fft_no_pdl = env_int("FB_FFT_NO_PDL", k.fft_no_pdl);
+    k.slab_fused = env_int("FB_SLAB_FUSED", k.slab_fused);
+    const char* pk = getenv("FB_ROWBLOCK_PANEL");
+    if (pk && pk[0]) k.rowblock_panel = atoll(pk);
+    k.f64_cfg = env_int("FB_F64_CFG", k.f64_cfg);
+    k.gemm_split2 = env_int("FB_GEMM_SPLIT2", k.gemm_split2);
+    k.gemm_splitv = env_int("FB_GEMM_SPLITV", k.gemm_splitv);
+    k.gemm_split_pdl = env_int("FB_GEMM_SPLIT_PDL", k.gemm_split_pdl);
+    k.gemm_1cta = env_int("FB_GEMM_1CTA", k.gemm_1cta);
+    k.bf16_cluster = env_int("FB_BF16_CLUSTER", k.bf16_cluster);
+    k.lu_tma = env_int("FB_LU_TMA", k.lu_tma);
+    k.lu_rank_simt = env_int("FB_LU_RANK_SIMT", k.lu_rank_simt);
+    k.lu_serial = env_int("FB_LU_SERIAL", k.lu_serial);
+    k.lu_lookahead = env_int("FB_LU_LOOKAHEAD", k.lu_lookahead);
+    k.lu_graph = env_int("FB_LU_GRAPH", k.lu_graph);
+#if FB_DEBUG_BUILD
+    k.fft_debug = env_int("FB_FFT_DEBUG", 0);
+    k.lu_debug = env_int("FB_LU_DEBUG", 0);
+#endif
+    return k;
+}
+static std::atomic<const Knobs*> g_knobs{nullptr};
+static std::mutex g_knobs_mu;
+void reload_knobs() {
+    std::lock_guard<std::mutex> lk(g_knobs_mu);
+    g_knobs.store(new Knobs(read_knobs()));  // the previous snapshot is kept alive (tiny, rare)
+}
+const Knobs& knobs() {
+    const Knobs* k = g_knobs.load();
+    if (!k) {
+        std::lock_guard<std::mutex> lk(g_knobs_mu);
+        if (!g_knobs.load()) g_knobs.store(new Knobs(read_knobs()));
+        k = g_knobs.load();
+    }
+    return *k;
+}
+
 static constexpr int kMaxDev = 64;
 static DeviceState g_dev[kMaxDev];
 static std::mutex g_dev_mu;
@@ -182,6 +242,8 @@ const char* fb_status_string(int s) {
 const char* fb_last_error_detail(void) { return t_err; }
 
 uint64_t fb_launch_count(void) { return g_launches.load(); }
+
+void fb_reload_knobs(void) { reload_knobs(); }
 
 fb_status fb_init(int device) {
     clear_error();

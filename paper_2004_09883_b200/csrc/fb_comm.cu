@@ -34,6 +34,7 @@ struct fb_comm {
     // row-block GEMM: panel broadcasts run on their own stream
     cudaStream_t cstream = nullptr;
     cudaEvent_t cev = nullptr;
+    int* flag_dev = nullptr;  // one int for the collective agreements (agree_min)
 };
 
 namespace fb {
@@ -120,8 +121,7 @@ static fb_status lsa_barrier(fb_comm* c, cudaStream_t s) {
 // Collective (called by every rank from fb_comm_init): decide whether the fused path is
 // available and create the device communicator with one LSA barrier.
 static void fused_probe(fb_comm* c) {
-    const char* e = getenv("FB_SLAB_FUSED");
-    if (e && e[0] == '0') {
+    if (knobs().slab_fused == 0) {
         snprintf(c->fused_why, sizeof(c->fused_why), "disabled by FB_SLAB_FUSED=0");
         return;
     }
@@ -149,26 +149,33 @@ static void fused_probe(fb_comm* c) {
     snprintf(c->fused_why, sizeof(c->fused_why), "fused (LSA team of %d)", c->size);
 }
 
-// Collective: (re)allocate and register the receive window, then map every rank's base.
-static fb_status ensure_window(fb_comm* c, size_t bytes) {
-    if (c->win_bytes >= bytes) return FB_OK;
-    if (c->win) {
-        FB_NCCL_TRY(ncclCommWindowDeregister(c->nccl, c->win), c->nccl);
-        c->win = nullptr;
-    }
-    if (c->win_buf) {
-        FB_NCCL_TRY(ncclMemFree(c->win_buf), c->nccl);
-        c->win_buf = nullptr;
-        c->win_bytes = 0;
-    }
-    FB_NCCL_TRY(ncclMemAlloc(&c->win_buf, bytes), c->nccl);
-    FB_NCCL_TRY(ncclCommWindowRegister(c->nccl, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC), c->nccl);
-    c->win_bytes = bytes;
+// Collective agreement: every rank contributes `ok`; returns the minimum over the world
+// (ncclAllReduce on the caller's stream, then a host sync).  Returns -1 if NCCL itself fails.
+static int agree_min(fb_comm* c, int ok, cudaStream_t s) {
+    if (!c->flag_dev && cudaMalloc(&c->flag_dev, sizeof(int)) != cudaSuccess) return -1;
+    int v = ok;
+    if (cudaMemcpyAsync(c->flag_dev, &v, sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess) return -1;
+    if (ncclAllReduce(c->flag_dev, c->flag_dev, 1, ncclInt32, ncclMin, c->nccl, s) != ncclSuccess) return -1;
+    if (cudaMemcpyAsync(&v, c->flag_dev, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess) return -1;
+    if (cudaStreamSynchronize(s) != cudaSuccess) return -1;
+    return v;
+}
+
+static void release_window(fb_comm* c) {
+    if (c->win) ncclCommWindowDeregister(c->nccl, c->win);
+    c->win = nullptr;
+    if (c->win_buf) ncclMemFree(c->win_buf);
+    c->win_buf = nullptr;
+    c->win_bytes = 0;
+}
+
+// Map every rank's window base (as seen from this GPU) into c->peer_base.
+static bool map_peers(fb_comm* c) {
     int lsa_of_rank[kMaxPeers];
     const ncclTeam_t world = ncclTeamWorld(c->nccl);
     for (int p = 0; p < c->size; ++p) lsa_of_rank[p] = ncclTeamRankToLsa(c->nccl, world, p);
     void* dbuf = nullptr;
-    FB_CUDA_TRY(cudaMalloc(&dbuf, kMaxPeers * (sizeof(void*) + sizeof(int))));
+    if (cudaMalloc(&dbuf, kMaxPeers * (sizeof(void*) + sizeof(int))) != cudaSuccess) return false;
     void** dptr = (void**)dbuf;
     int* dlsa = (int*)(dptr + kMaxPeers);
     cudaError_t ce = cudaMemcpy(dlsa, lsa_of_rank, c->size * sizeof(int), cudaMemcpyHostToDevice);
@@ -179,21 +186,58 @@ static fb_status ensure_window(fb_comm* c, size_t bytes) {
     void* host[kMaxPeers] = {};
     if (ce == cudaSuccess) ce = cudaMemcpy(host, dptr, c->size * sizeof(void*), cudaMemcpyDeviceToHost);
     cudaFree(dbuf);
-    if (ce != cudaSuccess) {
-        set_error("mapping the symmetric window failed: %s", cudaGetErrorString(ce));
-        return FB_ERR_CUDA;
-    }
+    if (ce != cudaSuccess) return false;
     for (int p = 0; p < c->size; ++p) c->peer_base[p] = (float2*)host[p];
+    return true;
+}
+
+// Collective (every rank makes the same slab calls, so every rank reaches this together with
+// the same `bytes`): (re)allocate and register the receive window and map every rank's base.
+// Each step that can fail on one rank alone is followed by an agreement (allreduce MIN of a
+// success flag), so either every rank ends with a mapped window or every rank releases its
+// part and switches to the ncclAlltoAll path -- no rank is left in a collective the others
+// skipped, and no rank pushes into a window a peer never mapped.  Growing the window first
+// quiesces the old one: this rank's stream is synchronised and the agreement doubles as a
+// barrier, so no peer still reads or writes the old window when it is freed.
+static fb_status ensure_window(fb_comm* c, size_t bytes, cudaStream_t s) {
+    if (c->win_bytes >= bytes) return FB_OK;
+    const char* why = nullptr;
+    if (c->win) {
+        const int q = (cudaStreamSynchronize(s) == cudaSuccess) ? 1 : 0;
+        if (agree_min(c, q, s) != 1) why = "quiescing the previous window failed";
+        release_window(c);
+    }
+    int ok = 0;
+    if (!why) {
+        ok = ncclMemAlloc(&c->win_buf, bytes) == ncclSuccess;
+        if (!ok) c->win_buf = nullptr;
+        if (agree_min(c, ok, s) != 1) why = "ncclMemAlloc failed on some rank";
+    }
+    if (!why) {  // collective registration: every rank has a buffer
+        ok = ncclCommWindowRegister(c->nccl, c->win_buf, bytes, &c->win, NCCL_WIN_COLL_SYMMETRIC) == ncclSuccess;
+        if (!ok) c->win = nullptr;
+        if (agree_min(c, ok, s) != 1) why = "ncclCommWindowRegister failed on some rank";
+    }
+    if (!why) {
+        ok = map_peers(c) ? 1 : 0;
+        if (agree_min(c, ok, s) != 1) why = "mapping the symmetric window failed on some rank";
+    }
+    if (why) {
+        release_window(c);
+        set_error("symmetric window of %zu bytes unavailable: %s", bytes, why);
+        return FB_ERR_NCCL;
+    }
+    c->win_bytes = bytes;
     return FB_OK;
 }
 
-// A window that cannot be allocated or registered (e.g. no symmetric-memory support for this
-// size) turns the communicator's fused path off for good; the call proceeds on ncclAlltoAll.
-static fb_status ensure_window_or_fallback(fb_comm* c, size_t bytes) {
-    const fb_status st = ensure_window(c, bytes);
+// A window that cannot be set up on every rank turns the communicator's fused path off for
+// good, on every rank at once (ensure_window agrees collectively); the call then proceeds on
+// ncclAlltoAll.
+static fb_status ensure_window_or_fallback(fb_comm* c, size_t bytes, cudaStream_t s) {
+    const fb_status st = ensure_window(c, bytes, s);
     if (st != FB_OK) {
-        snprintf(c->fused_why, sizeof(c->fused_why), "symmetric window of %zu bytes unavailable: %s", bytes,
-                 fb_last_error_detail());
+        snprintf(c->fused_why, sizeof(c->fused_why), "%s", fb_last_error_detail());
         clear_error();
     }
     return st;
@@ -287,6 +331,8 @@ fb_status fb_comm_destroy(fb_comm* c) {
     clear_error();
     if (!c) return FB_OK;
     fb_status st = FB_OK;
+    // the window may still be in use by this rank's queued work: drain the device first
+    if (c->win || c->win_buf) cudaDeviceSynchronize();
     if (c->nccl && c->win) {
         if (ncclCommWindowDeregister(c->nccl, c->win) != ncclSuccess) st = FB_ERR_NCCL;
         c->win = nullptr;
@@ -296,6 +342,7 @@ fb_status fb_comm_destroy(fb_comm* c) {
         c->win_buf = nullptr;
     }
     if (c->cev) cudaEventDestroy(c->cev);
+    if (c->flag_dev) cudaFree(c->flag_dev);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->nccl && c->devcomm_ok) {
         if (ncclDevCommDestroy(c->nccl, &c->devcomm) != ncclSuccess) st = FB_ERR_NCCL;
@@ -341,7 +388,7 @@ fb_status fb_fft2d_slab(fb_comm* c, const void* x_rows, void* y_cols, int64_t n0
     const size_t slab = (size_t)rows * n1;
     float2* send = (float2*)ws;
     float2* recv = send + slab;
-    if (c->fused && ensure_window_or_fallback(c, slab * sizeof(float2)) != FB_OK) c->fused = 0;
+    if (c->fused && ensure_window_or_fallback(c, slab * sizeof(float2), s) != FB_OK) c->fused = 0;
     if (c->fused) {
         FB_TRY(lsa_barrier(c, s));  // every peer is done with its window (previous call)
         FB_TRY(slab_rows_push((const float2*)x_rows, c->peer_base, c->rank, P, n0, n1, st, s));
@@ -378,7 +425,7 @@ fb_status fb_ifft2d_slab(fb_comm* c, const void* y_cols, void* x_rows, int64_t n
     const size_t slab = (size_t)rows * n1;
     float2* send = (float2*)ws;
     float2* recv = send + slab;
-    if (c->fused && ensure_window_or_fallback(c, slab * sizeof(float2)) != FB_OK) c->fused = 0;
+    if (c->fused && ensure_window_or_fallback(c, slab * sizeof(float2), s) != FB_OK) c->fused = 0;
     if (c->fused) {
         FB_TRY(lsa_barrier(c, s));  // no peer still reads this rank's window (previous call)
         FB_TRY(fft_columns((const float2*)y_cols, (float2*)c->win_buf, n0, cols, cols, cols, true, false, 1.f, send,
@@ -468,8 +515,7 @@ fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_
     const ncclDataType_t t = dtype == FB_F64 ? ncclDouble : ncclFloat;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t ml = m / c->size;
-    const char* pk_s = getenv("FB_ROWBLOCK_PANEL");  // K rows per broadcast panel (FP32 path)
-    const int64_t pk = pk_s ? atoll(pk_s) : 4096;
+    const int64_t pk = knobs().rowblock_panel;  // K rows per broadcast panel (FP32 path)
     if (dtype == FB_F32 && pk > 0 && pk < k) {
         // B is broadcast in contiguous K-row panels on a communication stream;
         // the operand split of A runs meanwhile, and each B panel is split (transposed to

@@ -47,6 +47,45 @@ extern std::atomic<uint64_t> g_launches;
         if (_s != FB_OK) return _s;       \
     } while (0)
 
+// ---------------------------------------------------------------- A/B knobs
+// Tuning switches for A/B measurements (defaults = the tuned configuration).  They are read
+// from the environment ONCE per process (first use, or fb_reload_knobs() -- the tests call it
+// after changing the environment); no launch path calls getenv.  Result-altering timing
+// decompositions (FB_FFT_DEBUG, FB_LU_DEBUG) are honoured only in builds compiled with
+// -DFB_DEBUG_BUILD=1 (tools), never in the product library.
+#ifndef FB_DEBUG_BUILD
+#define FB_DEBUG_BUILD 0
+#endif
+struct Knobs {
+    // FFT (fb_fft.cu, fb_fft_kern.cuh)
+    int fft_stagger_ns = 600, fft_col_stg = -1, fft_pair2 = 2, fft_colpair = 0, fft_col_max_log2 = 12;
+    int fft_4step_lb = -1, fft_pair = 1, fft_pair_max_log2 = 11, fft_no_tma_col = 0, fft_col_c = 0;
+    int fft_no_tma_row = 0, fft_col_nb = 0, fft_row_nb = 0, fft_no_tma = 0, fft_longrow = 1, fft_pair_tma = 1;
+    int fft_no_pdl = 0, fft_debug = 0;
+    // multi-GPU (fb_comm.cu)
+    int slab_fused = 1;
+    int64_t rowblock_panel = 4096;
+    // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
+    int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
+    // LU (fb_lu.cu)
+    int lu_tma = 1, lu_debug = 0, lu_rank_simt = 1, lu_serial = 0, lu_lookahead = 1, lu_graph = 1;
+};
+const Knobs& knobs();
+void reload_knobs();
+
+// Per-device "done once" bit mask for cudaFuncSetAttribute and similar per-context setup
+// (devices 0..31); atomic, so concurrent first calls at worst repeat the idempotent setup.
+struct DevOnce {
+    std::atomic<uint32_t> mask{0};
+    static int dev() {
+        int d = 0;
+        cudaGetDevice(&d);
+        return d & 31;
+    }
+    bool done(int d) const { return (mask.load() >> d) & 1u; }
+    void set(int d) { mask.fetch_or(1u << d); }
+};
+
 // Per-device immutable state (twiddle table pointer, SM count, ...).
 struct DeviceState {
     bool ready = false;

@@ -25,12 +25,13 @@ FB_FFT_EXTERN_L(10) FB_FFT_EXTERN_L(11) FB_FFT_EXTERN_L(12) FB_FFT_EXTERN_L(13) 
 fb_status launch_fft_pass(const FftPass& p_in, const DeviceState* st, cudaStream_t s) {
     if (p_in.nlines <= 0) return FB_OK;
     FftPass p = p_in;
-    p.debug = fft_knob("FB_FFT_DEBUG", 0);
-    p.stagger_ns = fft_knob("FB_FFT_STAGGER", 600);
+    const Knobs& kn = knobs();
+    p.debug = kn.fft_debug;  // 0 unless built with FB_DEBUG_BUILD
+    p.stagger_ns = kn.fft_stagger_ns;
     p.sm_count = st->sm_count;
-    p.col_stg = fft_knob("FB_FFT_COL_STG", -1);
-    p.pair_half_shfl = fft_knob("FB_FFT_PAIR2", 2);
-    p.col_pair_last = fft_knob("FB_FFT_COLPAIR", 0);
+    p.col_stg = kn.fft_col_stg;
+    p.pair_half_shfl = kn.fft_pair2;
+    p.col_pair_last = kn.fft_colpair;
     switch (p.log2L) {
         case 0: return launch_pass_L<0>(p, st, s);
         case 1: return launch_pass_L<1>(p, st, s);
@@ -64,7 +65,7 @@ static LineMap plain_map(int64_t hi, int64_t lo, int64_t es) {
 
 // column lines up to 2^12 in one pass (knob FB_FFT_COL_MAX_LOG2 for A/B; longer ones use the
 // four-step split)
-static int max_onchip_col() { return fft_knob("FB_FFT_COL_MAX_LOG2", 12); }
+static int max_onchip_col() { return knobs().fft_col_max_log2; }
 
 fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, int64_t ld_in,
                       int64_t ld_out, bool conj_in, bool conj_out, float scale, float2* tmp,
@@ -107,7 +108,7 @@ fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, 
         set_error("internal: four-step column FFT needs a workspace");
         return FB_ERR_WORKSPACE;
     }
-    const int lb = fft_knob("FB_FFT_4STEP_LB", l0 >= 14 ? 7 : (l0 + 1) / 2);
+    const int lb = knobs().fft_4step_lb > 0 ? knobs().fft_4step_lb : (l0 >= 14 ? 7 : (l0 + 1) / 2);
     const int la = l0 - lb;
     const int64_t a = int64_t(1) << la, b = int64_t(1) << lb;
     FftPass p1{};
@@ -146,7 +147,7 @@ fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, 
 // cost 22 us, 32-byte rows 16.5 us).  Needs an n0 x n1 workspace (out-of-place column pass).
 static bool use_pair_plan(int64_t n0, int64_t n1) {
     const int l0 = ilog2(n0), l1 = ilog2(n1);
-    return fft_knob("FB_FFT_PAIR", 1) != 0 && l0 >= 9 && l0 <= fft_knob("FB_FFT_PAIR_MAX_LOG2", 11) &&
+    return knobs().fft_pair != 0 && l0 >= 9 && l0 <= knobs().fft_pair_max_log2 &&
            l0 <= max_onchip_col() && l1 >= 6 && l1 <= 12;
 }
 

@@ -535,13 +535,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
     }
 }
 
-// Tuning knobs read once from the environment (for A/B measurements; defaults are the tuned
-// configuration).
-static int fft_knob(const char* name, int dflt) {
-    const char* e = getenv(name);
-    return (e && e[0]) ? atoi(e) : dflt;
-}
-static bool fft_pdl_enabled() { return fft_knob("FB_FFT_NO_PDL", 0) == 0; }
+static bool fft_pdl_enabled() { return knobs().fft_no_pdl == 0; }
 
 // Launch with programmatic stream serialization: the kernel may start while the previous
 // kernel on the stream drains; every FFT kernel calls pdl_wait() before touching global memory.
@@ -568,13 +562,12 @@ static fb_status launch_one(const FftPass& p, const DeviceState* st, cudaStream_
     constexpr int threads = C * G::T;
     static_assert(threads <= 1024, "CTA too large");
     const size_t smem = (G::NSTAGES > 1) ? (size_t)C * G::PADL * sizeof(float2) : 0;
-    static int attr_done_mask = 0;  // per-device bit (devices 0..31)
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (smem > 48 * 1024 && !(attr_done_mask & (1 << (dev & 31)))) {
+    static DevOnce once;
+    const int dev = DevOnce::dev();
+    if (smem > 48 * 1024 && !once.done(dev)) {
         FB_CUDA_TRY(cudaFuncSetAttribute(fft_pass_kernel<LOG2L, C, MODE>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        attr_done_mask |= 1 << (dev & 31);
+        once.set(dev);
     }
     const int64_t blocks = (p.nlines + C - 1) / C;
     if (blocks > 0x7fffffff) {
@@ -729,7 +722,8 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
         }
     };
 
-    const bool dbg_noload = (p.debug & 2) != 0;
+    const int dbg = FB_DEBUG_BUILD ? p.debug : 0;  // timing decomposition (debug builds only)
+    const bool dbg_noload = (dbg & 2) != 0;
     if (tid == 0 && !dbg_noload) {
         // Staggered start: CTA slot s (the s-th CTA placed on an SM) issues its first load
         // s * stagger_ns later, so the slot-0 CTAs get their first group from a less crowded
@@ -786,7 +780,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
 
         if constexpr (KIND == KIND_ROW && C == 2 && !OUT_GENERIC && PairLast<LOG2L>::ok) {
             if (p.pair_log2N > 0 && p.pair_half_shfl == 2 && p.tw4_log2N == 0 && !p.conj_out && p.scale == 1.0f &&
-                !p.debug) {
+                !dbg) {
                 Stages<LOG2L, C, 0, PairLast<LOG2L>::S>::run(v, X, t, c, stw, nullptr);
                 const int64_t gq = (grp * C) >> ((gshift >= 62) ? 62 : gshift);
                 float2* row0 = p.out + gq * p.lout.hi;
@@ -795,7 +789,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
             }
         }
         if constexpr (KIND == KIND_COL && ColPairLast<LOG2L, C>::ok) {
-            if (p.col_pair_last && !p.col_stg && p.tw4_log2N == 0 && p.pair_log2N == 0 && !p.debug) {
+            if (p.col_pair_last && !p.col_stg && p.tw4_log2N == 0 && p.pair_log2N == 0 && !dbg) {
                 Stages<LOG2L, C, 0, ColPairLast<LOG2L, C>::S>::run(v, X, t, c, stw, nullptr);
                 ColPairLast<LOG2L, C>::run(X, t, c, stw, p.conj_out, p.scale);
                 ptx::fence_proxy_async_smem();
@@ -812,8 +806,8 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
                 continue;
             }
         }
-        if (!(p.debug & 1)) Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
-        if (p.debug & 4) continue;
+        if (!(dbg & 1)) Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
+        if (dbg & 4) continue;
 
         const int64_t g = grp * C + c;
         const int64_t gh = (gshift >= 62) ? 0 : (g >> gshift);
@@ -949,19 +943,18 @@ static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStr
     using TG = TmaGeom<LOG2L, C, KIND, NB>;
     constexpr int threads = C * LineGeom<LOG2L>::T;
     auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC, NB>;
-    static int attr_done_mask = 0;
-    static int occ[32] = {0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(attr_done_mask & (1 << (dev & 31)))) {
+    static DevOnce once;
+    static std::atomic<int> occ[32];
+    const int dev = DevOnce::dev();
+    if (!once.done(dev)) {
         FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG::SMEM));
         int nb = 0;
         FB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, TG::SMEM));
-        occ[dev & 31] = nb < 1 ? 1 : nb;
-        attr_done_mask |= 1 << (dev & 31);
+        occ[dev].store(nb < 1 ? 1 : nb);
+        once.set(dev);
     }
     const int64_t ngroups = (p.nlines + C - 1) / C;
-    int64_t grid = (int64_t)st->sm_count * occ[dev & 31];
+    int64_t grid = (int64_t)st->sm_count * occ[dev].load();
     if (grid > ngroups) grid = ngroups;
     CUtensorMap tin, tout;
     memset(&tin, 0, sizeof(tin));
@@ -1001,11 +994,11 @@ static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic)
     const bool in_plain = p.lin.kb_shift >= l, out_plain = p.lout.kb_shift >= l;
     const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
     if (p.col_like && p.lin.lo == 1 && p.lout.lo == 1 && in_plain && out_plain) {
-        if (fft_knob("FB_FFT_NO_TMA_COL", 0)) return false;
+        if (knobs().fft_no_tma_col) return false;
         // widest row segment (up to 128 B = 16 columns) whose double-buffered staging plus
         // exchange buffer stays near 100 KiB (two CTAs per SM)
         C = (l <= 8) ? 16 : (l == 9 ? 8 : (l == 10 ? 4 : 2));
-        const int kc = fft_knob("FB_FFT_COL_C", 0);
+        const int kc = knobs().fft_col_c;
         if (kc == 2 || kc == 4 || kc == 8 || kc == 16) C = kc;
         if (C * (1 << l) / 16 > 1024 || (size_t)C * (1 << l) * 8 * 3 > 200 * 1024) return false;
         const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
@@ -1022,7 +1015,7 @@ static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic)
     const bool lo_ok = (p.lout.lo == 0 && p.lin.lo == 0) ||
                        (p.pair_log2N > 0 && (p.lin.lo * 8) % 16 == 0 && (p.lout.lo * 8) % 16 == 0);
     if (!p.col_like && p.lin.es == 1 && lo_ok) {
-        if (fft_knob("FB_FFT_NO_TMA_ROW", 0)) return false;
+        if (knobs().fft_no_tma_row) return false;
         const int seg = in_plain ? (1 << l) : (1 << p.lin.kb_shift);
         if (seg < 2) return false;
         if ((p.lin.hi * 8) % 16) return false;
@@ -1041,7 +1034,7 @@ static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic)
 // 3.05); with fewer groups per CTA (<= 1024^2) two buffers and 2 CTAs/SM avoid a serial
 // second group on a third of the CTAs (17.4 us vs 19.0 at 1024^2).  Knob (1 or 2) forces.
 template <int LOG2L, int C, int KIND>
-static fb_status launch_tma_nb(const FftPass& p, const DeviceState* st, cudaStream_t s, const char* knob) {
+static fb_status launch_tma_nb(const FftPass& p, const DeviceState* st, cudaStream_t s, int knob_nb) {
     constexpr int D = tma_nb<LOG2L, C, KIND>();
     int nb = D;
     if constexpr (D == 1) {
@@ -1049,7 +1042,7 @@ static fb_status launch_tma_nb(const FftPass& p, const DeviceState* st, cudaStre
         const int64_t ngroups = (p.nlines + C - 1) / C;
         if (ngroups < 2 * (int64_t)st->sm_count * (occ1 < 3 ? occ1 : 3)) nb = 2;
     }
-    nb = fft_knob(knob, nb);
+    if (knob_nb == 1 || knob_nb == 2) nb = knob_nb;
     if (nb == 3 - D) return launch_tma_one<LOG2L, C, KIND, false, 3 - D>(p, st, s);
     return launch_tma_one<LOG2L, C, KIND, false, D>(p, st, s);
 }
@@ -1058,22 +1051,22 @@ template <int LOG2L>
 static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const DeviceState* st, cudaStream_t s) {
     constexpr int T = LineGeom<LOG2L>::T;
     if (kind == KIND_COL) {
-        if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
-        if (C == 4) return launch_tma_nb<LOG2L, 4, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+        if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_COL>(p, st, s, knobs().fft_col_nb);
+        if (C == 4) return launch_tma_nb<LOG2L, 4, KIND_COL>(p, st, s, knobs().fft_col_nb);
         if constexpr (8 * T <= 1024 && LOG2L <= 11)
-            if (C == 8) return launch_tma_nb<LOG2L, 8, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+            if (C == 8) return launch_tma_nb<LOG2L, 8, KIND_COL>(p, st, s, knobs().fft_col_nb);
         if constexpr (16 * T <= 1024 && LOG2L <= 10)
-            if (C == 16) return launch_tma_nb<LOG2L, 16, KIND_COL>(p, st, s, "FB_FFT_COL_NB");
+            if (C == 16) return launch_tma_nb<LOG2L, 16, KIND_COL>(p, st, s, knobs().fft_col_nb);
     } else {
-        if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_ROW>(p, st, s, "FB_FFT_ROW_NB");
-        if (!og) return launch_tma_nb<LOG2L, 1, KIND_ROW>(p, st, s, "FB_FFT_ROW_NB");
+        if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_ROW>(p, st, s, knobs().fft_row_nb);
+        if (!og) return launch_tma_nb<LOG2L, 1, KIND_ROW>(p, st, s, knobs().fft_row_nb);
         return launch_tma_one<LOG2L, 1, KIND_ROW, true>(p, st, s);
     }
     set_error("internal: no TMA FFT instantiation");
     return FB_ERR_UNSUPPORTED_SIZE;
 }
 
-static bool g_fft_tma_disabled() { return fft_knob("FB_FFT_NO_TMA", 0) == 1; }
+static bool g_fft_tma_disabled() { return knobs().fft_no_tma == 1; }
 
 
 // =====================================================================================
@@ -1168,19 +1161,18 @@ static bool longrow_eligible(const FftPass& p) {
     if (p.g_shift != 0 && p.g_shift < 62) return false;
     if (p.lin.es != 1 || p.lin.kb_shift < 14 || p.lout.es != 1) return false;
     if (((uintptr_t)p.in & 15) || ((uintptr_t)p.out & 15) || (p.lin.hi * 8) % 16) return false;
-    return fft_knob("FB_FFT_LONGROW", 1) != 0 && !g_fft_tma_disabled();
+    return knobs().fft_longrow != 0 && !g_fft_tma_disabled();
 }
 
 template <bool OG>
 static fb_status launch_longrow(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     using G = LineGeom<14>;
     constexpr size_t SMEM = (size_t)(G::PADL + G::L / 2) * sizeof(float2) + 64;
-    static int attr_mask = 0;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(attr_mask & (1 << (dev & 31)))) {
+    static DevOnce once;
+    const int dev = DevOnce::dev();
+    if (!once.done(dev)) {
         FB_CUDA_TRY(cudaFuncSetAttribute(fft_longrow_kernel<OG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
-        attr_mask |= 1 << (dev & 31);
+        once.set(dev);
     }
     int64_t grid = st->sm_count;
     if (grid > p.nlines) grid = p.nlines;
@@ -1200,7 +1192,7 @@ fb_status launch_pass_L(const FftPass& p, const DeviceState* st, cudaStream_t s)
         // pass is expressible (A/B at 2048^2: 22 us vs 28 us for the plain kernel with C = 2);
         // FB_FFT_PAIR_TMA=0 forces the plain kernel.
         if constexpr (has_tma) {
-            if (fft_knob("FB_FFT_PAIR_TMA", 1) && !g_fft_tma_disabled() && tma_eligible(p, kind, tc, og) && tc == 2 &&
+            if (knobs().fft_pair_tma && !g_fft_tma_disabled() && tma_eligible(p, kind, tc, og) && tc == 2 &&
                 !og)
                 return launch_tma_L<LOG2L>(p, kind, tc, og, st, s);
         }

@@ -770,7 +770,7 @@ template <class CF>
 static fb_status launch_f64(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
                             void* C, int64_t ldc, cudaStream_t s) {
     auto kern = f64::gemm_f64_dmma_kernel<CF>;
-    static int attr_mask = 0;
+    static std::atomic<int> attr_mask{0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_mask & (1 << (dev & 31)))) {
@@ -792,7 +792,7 @@ fb_status gemm_f64_sub_device(int64_t m, int64_t n, int64_t k, const double* A, 
                               int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
     using CF = f64::CfgSmall;
     auto kern = f64::gemm_f64_dmma_kernel<CF, true>;
-    static int attr_mask = 0;
+    static std::atomic<int> attr_mask{0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_mask & (1 << (dev & 31)))) {
@@ -816,8 +816,7 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
                       const void* B, int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
                       const DeviceState* st, cudaStream_t s) {
     if (dtype == FB_F64) {
-        const char* kv = getenv("FB_F64_CFG");  // A/B knob: 0 = 64x64 (default), 1 = 128x128, 2 = 128x64
-        const int cfg = kv ? atoi(kv) : 0;
+        const int cfg = knobs().f64_cfg;  // A/B knob: 0 = 64x64 (default), 1 = 128x128, 2 = 128x64
         if (cfg == 1) return launch_f64<f64::Cfg<128, 128, 2, 4>>(m, n, k, A, lda, B, ldb, C, ldc, s);
         if (cfg == 2) return launch_f64<f64::Cfg<128, 64, 2, 2>>(m, n, k, A, lda, B, ldb, C, ldc, s);
         return launch_f64<f64::CfgSmall>(m, n, k, A, lda, B, ldb, C, ldc, s);
@@ -836,11 +835,10 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
     float* Al = Ah + m * kp;
     float* Bh = Al + m * kp;
     float* Bl = Bh + n * kp;
-    const char* sk = getenv("FB_GEMM_SPLIT2");  // A/B knob: 1 = two split launches
-    if (sk && sk[0] == '1') {
+    if (knobs().gemm_split2 == 1) {  // A/B knob: 1 = two split launches
         FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
         FB_TRY(tf32_split_device(1, k, n, (const float*)B, ldb, Bh, Bl, kp, st, s));
-    } else if (!(getenv("FB_GEMM_SPLITV") && getenv("FB_GEMM_SPLITV")[0] == '1') &&
+    } else if (knobs().gemm_splitv != 1 &&
                m * ((k + 3) / 4) + 1024 < INT32_MAX) {
         // default: the wide split (A/B knob FB_GEMM_SPLITV=1: split_both_kernel)
         const int64_t nblk_a = (m * ((k + 3) / 4) + 1023) / 1024;
@@ -851,7 +849,7 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
         }
         tf32::split_both_wide_kernel<<<(unsigned)(nblk_a + nblk_b), 256, 0, s>>>(
             (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a,
-            (getenv("FB_GEMM_SPLIT_PDL") && getenv("FB_GEMM_SPLIT_PDL")[0] == '1') ? 1 : 0);
+            knobs().gemm_split_pdl == 1 ? 1 : 0);
         FB_LAUNCH_CHECK("split_both_wide_kernel");
     } else {
         const int a_cblk = (int)((((k + 3) / 4) + 255) / 256);
@@ -895,11 +893,10 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
     FB_TRY(tf32::make_kmajor_map(&mAl, Al, m, k, lda, tf32::BM));
     FB_TRY(tf32::make_kmajor_map(&mBh, Bh, n, k, ldb, tf32::BN));
     FB_TRY(tf32::make_kmajor_map(&mBl, Bl, n, k, ldb, tf32::BN));
-    static int attr_mask = 0;
+    static std::atomic<int> attr_mask{0};
     int dev = 0;
     cudaGetDevice(&dev);
-    const char* knob = getenv("FB_GEMM_1CTA");
-    const bool one_cta = knob && knob[0] == '1';
+    const bool one_cta = knobs().gemm_1cta == 1;
     if (!(attr_mask & (1 << (dev & 31)))) {
         FB_CUDA_TRY(cudaFuncSetAttribute(tf32::gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tf32::SMEM));

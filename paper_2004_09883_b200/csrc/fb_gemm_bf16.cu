@@ -306,9 +306,8 @@ fb_status fb_matmul_bf16(int64_t m, int64_t n, int64_t k, const void* A, int64_t
     FB_TRY(bf16::kmajor_map(&mB, Bt, n, k, ldbt));
     // A/B knob FB_BF16_CLUSTER=4: two pairs per cluster with the A tiles multicast (correct, but
     // measured slower at 8192^3: 1227 vs 1312 TFLOP/s -- operand traffic is not the limit)
-    const char* ck = getenv("FB_BF16_CLUSTER");
-    const int CLn = (ck && ck[0] == '4') ? 4 : 2;
-    static int attr_mask = 0;
+    const int CLn = knobs().bf16_cluster == 4 ? 4 : 2;
+    static std::atomic<int> attr_mask{0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_mask & (1 << (dev & 31)))) {

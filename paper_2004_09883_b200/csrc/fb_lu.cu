@@ -802,13 +802,14 @@ size_t lu_ws_bytes(int64_t) { return 0; }
 // before touching the matrix, so its launch overlaps the previous kernel's tail).
 template <typename Kern, typename... Args>
 static fb_status lu_launch(Kern kern, dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
-    static bool attr_set = false;
-    if (smem > 48 * 1024 && !attr_set) {
+    static DevOnce once;  // the attribute is per device context
+    const int dev = DevOnce::dev();
+    if (smem > 48 * 1024 && !once.done(dev)) {
         FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_kernel<512, 4, lu::NB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 2048 * lu::NB * 8));
         FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_kernel<1024, 4, lu::NB / 2>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 4096 * (lu::NB / 2) * 8));
-        attr_set = true;
+        once.set(dev);
     }
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -887,13 +888,14 @@ static fb_status lu_tensor_map(CUtensorMap* m, double* A, int64_t n, int64_t lda
 
 template <int PT, int RPT, int PNB>
 static fb_status lu_la_attrs() {  // outside any stream capture
-    static bool attr = false;
-    if (!attr) {
+    static DevOnce once;  // the attribute is per device context
+    const int dev = DevOnce::dev();
+    if (!once.done(dev)) {
         FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_la_kernel<PT, RPT, PNB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
         FB_CUDA_TRY(cudaFuncSetAttribute(lu::lu_panel_tma_kernel<PT, RPT, PNB>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-        attr = true;
+        once.set(dev);
     }
     return FB_OK;
 }
@@ -904,19 +906,18 @@ static fb_status lu_device_la(int64_t n, double* A, int64_t lda, int32_t* ipiv, 
     auto panel = lu::lu_panel_la_kernel<PT, RPT, PNB>;
     auto panel_tma = lu::lu_panel_tma_kernel<PT, RPT, PNB>;
     FB_TRY((lu_la_attrs<PT, RPT, PNB>()));
-    const char* tk = getenv("FB_LU_TMA");  // A/B knob: 0 = cp.async panel kernel
-    const bool use_tma = !(tk && tk[0] == '0') && (lda * 8) % 16 == 0 && ((uintptr_t)A & 15) == 0;
+    const Knobs& kn = knobs();
+    // A/B knob FB_LU_TMA=0: cp.async panel kernel
+    const bool use_tma = kn.lu_tma != 0 && (lda * 8) % 16 == 0 && ((uintptr_t)A & 15) == 0;
     CUtensorMap tmA;
     memset(&tmA, 0, sizeof(tmA));
     if (use_tma) FB_TRY(lu_tensor_map(&tmA, A, n, lda, PNB));
     LuStreams* ls;
     FB_TRY(lu_streams(&ls));
-    const char* dbg_s = getenv("FB_LU_DEBUG");  // timing decomposition only (wrong results): 1 no GEMM, 2 no swap/TRSM, 4 no panel
-    const int dbg = dbg_s ? atoi(dbg_s) : 0;
-    const char* rs_s = getenv("FB_LU_RANK_SIMT");  // A/B knob: 0 = DMMA GEMM for the trailing update
-    const bool rank_simt = !(rs_s && rs_s[0] == '0');
-    const char* ser = getenv("FB_LU_SERIAL");  // debug knob: run the wide parts on the caller's stream
-    cudaStream_t wst = (ser && ser[0] == '1') ? s : ls->w;
+    // timing decomposition (FB_DEBUG_BUILD only; wrong results): 1 no GEMM, 2 no swap/TRSM, 4 no panel
+    const int dbg = FB_DEBUG_BUILD ? kn.lu_debug : 0;
+    const bool rank_simt = kn.lu_rank_simt != 0;  // A/B knob FB_LU_RANK_SIMT=0: DMMA GEMM trailing update
+    cudaStream_t wst = kn.lu_serial == 1 ? s : ls->w;  // A/B knob: the wide parts on the caller's stream
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));
     FB_CUDA_TRY(cudaEventRecord(ls->ev_fork, s));
     FB_CUDA_TRY(cudaStreamWaitEvent(ls->w, ls->ev_fork, 0));  // w starts after everything before the call
@@ -1036,10 +1037,8 @@ static fb_status lu_device_graph(int64_t n, double* A, int64_t lda, int32_t* ipi
 }
 
 fb_status lu_device(int64_t n, double* A, int64_t lda, int32_t* ipiv, int32_t* info, cudaStream_t s) {
-    const char* la = getenv("FB_LU_LOOKAHEAD");
-    if (!(la && la[0] == '0')) {
-        const char* gk = getenv("FB_LU_GRAPH");
-        if (!(gk && gk[0] == '0')) return lu_device_graph(n, A, lda, ipiv, info, s);
+    if (knobs().lu_lookahead != 0) {
+        if (knobs().lu_graph != 0) return lu_device_graph(n, A, lda, ipiv, info, s);
         return lu_device_la_any(n, A, lda, ipiv, info, s);
     }
     FB_CUDA_TRY(cudaMemsetAsync(info, 0, sizeof(int32_t), s));

@@ -71,6 +71,26 @@ def uniform_pm1(count: int, tensor_id: int, start: int = 0, seed: int = SEED,
     return out
 
 
+def uniform_pm1_f64(count: int, tensor_id: int, start: int = 0, seed: int = SEED) -> np.ndarray:
+    """float64 values in [-1,1) with a FULL 53-bit mantissa draw (top 53 bits of the same
+    SplitMix64 stream): products of two such values are not exact in FP64, so an FP64 GEMM
+    test on them probes the rounding of every product, not only the accumulation order."""
+    st = np.uint64(stream_seed(tensor_id, seed))
+    out = np.empty(count, dtype=np.float64)
+    for c0 in range(0, count, _CHUNK):
+        c1 = min(count, c0 + _CHUNK)
+        with np.errstate(over="ignore"):
+            idx = np.arange(start + c0, start + c1, dtype=np.uint64) + st
+        u = (mix64(idx) >> np.uint64(11)).astype(np.int64)  # top 53 bits
+        out[c0:c1] = (u - (1 << 52)).astype(np.float64) * 2.0 ** -52
+    return out
+
+
+def real_matrix_f64(m: int, n: int, tensor_id: int, seed: int = SEED) -> np.ndarray:
+    """m x n float64 matrix of full-mantissa values in [-1, 1) (see uniform_pm1_f64)."""
+    return uniform_pm1_f64(m * n, tensor_id, seed=seed).reshape(m, n)
+
+
 def complex_field(n0: int, n1: int, tensor_id: int = TID_FFT_X, row0: int = 0,
                   rows: int | None = None, seed: int = SEED) -> np.ndarray:
     """complex64 [rows, n1] slice (rows row0..row0+rows) of the global n0 x n1 field."""

@@ -108,6 +108,19 @@ def test_2048_config1_sampled_and_closed_forms(fb):
     assert oracle.rel_l2(z, x) < 5e-7
 
 
+def test_2048_config1_full_oracle_fwd_inv(fb):
+    """BASELINE configs[1] at its full size against the FULL oracle (every output element), in
+    the launch configuration bench.py times: forward, and inverse of the forward's output."""
+    n = 2048
+    x = synth.complex_field(n, n)
+    y = _run(fb, x)
+    e_fwd = oracle.rel_l2(y, oracle.dft2d(x))
+    z = _run(fb, y, inverse=True)
+    e_inv = oracle.rel_l2(z, oracle.dft2d(y, inverse=True))
+    print(f"2048^2 full oracle: forward {e_fwd:.3e} inverse {e_inv:.3e}")
+    assert e_fwd < 5e-7 and e_inv < 5e-7
+
+
 def test_2048_tones(fb):
     """Paper-shaped input (P:149 vibration analysis): integer tones + noise; the spectrum
     peaks sit exactly at the tone frequencies."""
@@ -131,11 +144,15 @@ def test_four_step_columns(fb, n0, n1):
 
 
 def test_16384_square_sampled(fb):
-    """configs[3] size on one GPU: 16384 x 16384 (2 GiB), sampled lines + tone closed form."""
+    """configs[3] size on one GPU: 16384 x 16384 (2 GiB): 16 full output rows and 16 full output
+    columns against the oracle -- the first and last line of every slab at P = 8 (which include
+    those of P = 2 and 4), for both the row slabs and the column slabs -- plus the tone closed form."""
     n = 16384
     x = synth.complex_field(n, n)
     y = _run(fb, x)
-    _sampled_check(fb, n, n, x, y, [0, n - 1], [0, 8191], tol=1e-6)
+    edges = sorted({b for r in range(8) for b in (r * n // 8, (r + 1) * n // 8 - 1)})
+    assert len(edges) == 16
+    _sampled_check(fb, n, n, x, y, edges, edges, tol=1e-6)
     # single tone: exact spike at (f0, f1)
     f0, f1 = 1234, 15000
     i = np.arange(n, dtype=np.int64)

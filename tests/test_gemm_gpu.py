@@ -32,22 +32,48 @@ SHAPES = [(1, 1, 1), (1, 4, 4), (4, 4, 1), (16, 16, 16), (128, 128, 32), (130, 1
           (511, 384, 257), (1000, 40, 1030), (64, 1024, 8), (300, 300, 4)]
 
 
+def _mm_padded(fb, A, B):
+    """A (m x k) and B (k x n) in buffers whose rows are padded to 16 bytes (the C-ABI rule
+    ld*elemsize % 16 == 0), passed as strided views; C likewise.  Ragged k and n then run."""
+    es = A.itemsize
+    q = 16 // es
+    m, k = A.shape
+    n = B.shape[1]
+    dt = torch.float32 if es == 4 else torch.float64
+    Ab = torch.zeros(m, -(-k // q) * q, dtype=dt)
+    Bb = torch.zeros(k, -(-n // q) * q, dtype=dt)
+    Ab[:, :k] = torch.from_numpy(A)
+    Bb[:, :n] = torch.from_numpy(B)
+    Ab, Bb = Ab.cuda(), Bb.cuda()
+    Cb = torch.full((m, Bb.shape[1]), 7.0, dtype=dt, device="cuda")
+    fb.matmul(Ab[:, :k], Bb[:, :n], out=Cb[:, :n])
+    torch.cuda.synchronize()
+    assert torch.all(Cb[:, n:] == 7.0)  # padding columns of C untouched
+    return Cb[:, :n].cpu().numpy()
+
+
 @pytest.mark.parametrize("m,n,k", SHAPES)
 def test_f64_ragged_vs_oracle(fb, m, n, k):
     A = synth.real_matrix(m, k, synth.TID_GEMM_A, dtype=np.float64)
     B = synth.real_matrix(k, n, synth.TID_GEMM_B, dtype=np.float64)
-    if n % 2 or k % 2:
-        pytest.skip("FP64 rows must be 16-byte multiples for the C ABI (ld*8 % 16)")
-    assert oracle.rel_l2(_mm(fb, A, B), oracle.matmul(A, B)) < 1e-12
+    assert oracle.rel_l2(_mm_padded(fb, A, B), oracle.matmul(A, B)) < 1e-12
 
 
 @pytest.mark.parametrize("m,n,k", SHAPES)
 def test_f32_ragged_vs_oracle(fb, m, n, k):
-    if n % 4 or k % 4:
-        pytest.skip("FP32 rows must be 16-byte multiples for the C ABI (ld*4 % 16)")
     A = synth.real_matrix(m, k, synth.TID_GEMM_A)
     B = synth.real_matrix(k, n, synth.TID_GEMM_B)
-    assert oracle.rel_l2(_mm(fb, A, B), oracle.matmul(A, B)) < 1e-5
+    assert oracle.rel_l2(_mm_padded(fb, A, B), oracle.matmul(A, B)) < 1e-5
+
+
+@pytest.mark.parametrize("m,n,k", [(255, 260, 300), (2048, 2048, 2048), (130, 132, 36)])
+def test_f64_full_mantissa_vs_oracle(fb, m, n, k):
+    """Full 53-bit-mantissa inputs: every product rounds, so the 1e-12 bar probes the DMMA
+    products and the accumulation, not only the summation order (24-bit inputs multiply exactly)."""
+    A = synth.real_matrix_f64(m, k, synth.TID_GEMM_A)
+    B = synth.real_matrix_f64(k, n, synth.TID_GEMM_B)
+    err = oracle.rel_l2(_mm(fb, A, B), oracle.matmul(A, B))
+    assert err < 1e-12, err
 
 
 def test_f32_padded_leading_dims(fb):
@@ -186,6 +212,30 @@ def test_gemm_ex_transposes_alpha_beta(fb, dt, ta, tb):
         torch.cuda.synchronize()
         ref = alpha * P + beta * C0.astype(np.float64)
         assert oracle.rel_l2(C.cpu().numpy(), ref) < bar, (alpha, beta)
+
+
+@pytest.mark.parametrize("ta,tb,m,n,k", [(1, 0, 128, 128, 6), (1, 1, 96, 40, 13), (0, 0, 100, 130, 64),
+                                         (0, 1, 64, 130, 50), (1, 0, 33, 131, 7)])
+def test_gemm_ex_f32_unaligned_temporaries(fb, ta, tb, m, n, k):
+    """fb_gemm FP32 with k % 4 != 0 under transA (the transposed copy of A gets a 16-byte row
+    pitch) and n % 4 != 0, n >= 128 with (alpha, beta) != (1, 0) (the product tile T gets a
+    16-byte row pitch): every operand and C live in 16-byte-pitched buffers, as the ABI requires."""
+    q = 4
+    def padded(rows, cols, tid):
+        h = synth.real_matrix(rows, cols, tid)
+        b = torch.zeros(rows, -(-cols // q) * q)
+        b[:, :cols] = torch.from_numpy(h)
+        return h, b.cuda()[:, :cols]
+    Ah, A = padded(k if ta else m, m if ta else k, synth.TID_GEMM_A)
+    Bh, B = padded(n if tb else k, k if tb else n, synth.TID_GEMM_B)
+    C0h, C = padded(m, n, synth.TID_NOISE)
+    opA = Ah.T if ta else Ah
+    opB = Bh.T if tb else Bh
+    P = oracle.matmul(np.ascontiguousarray(opA).astype(np.float64), np.ascontiguousarray(opB).astype(np.float64))
+    alpha, beta = 0.75, -0.5
+    fb.gemm(A, B, C, alpha, beta, bool(ta), bool(tb))
+    torch.cuda.synchronize()
+    assert oracle.rel_l2(C.cpu().numpy(), alpha * P + beta * C0h.astype(np.float64)) < 1e-5
 
 
 def test_gemm_ex_beta0_ignores_nan_and_alpha0(fb):
