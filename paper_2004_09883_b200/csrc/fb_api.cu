@@ -43,6 +43,7 @@ static Knobs read_knobs() {
     k.fft_longrow = env_int("FB_FFT_LONGROW", k.fft_longrow);
     k.fft_pair_tma = env_int("FB_FFT_PAIR_TMA", k.fft_pair_tma);
     k.fft_no_pdl = env_int("FB_FFT_NO_PDL", k.fft_no_pdl);
+    k.fft_sub = env_int("FB_FFT_SUB", k.fft_sub);
     k.slab_fused = env_int("FB_SLAB_FUSED", k.slab_fused);
     const char* pk = getenv("FB_ROWBLOCK_PANEL");
     if (pk && pk[0]) k.rowblock_panel = atoll(pk);

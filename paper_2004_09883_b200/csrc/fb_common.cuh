@@ -61,7 +61,7 @@ struct Knobs {
     int fft_stagger_ns = 600, fft_col_stg = -1, fft_pair2 = 2, fft_colpair = 0, fft_col_max_log2 = 12;
     int fft_4step_lb = -1, fft_pair = 1, fft_pair_max_log2 = 11, fft_no_tma_col = 0, fft_col_c = 0;
     int fft_no_tma_row = 0, fft_col_nb = 0, fft_row_nb = 0, fft_no_tma = 0, fft_longrow = 1, fft_pair_tma = 1;
-    int fft_no_pdl = 0, fft_debug = 0;
+    int fft_no_pdl = 0, fft_debug = 0, fft_sub = 0;  // FB_FFT_SUB: 0 auto, 1 / 3 forced
     // multi-GPU (fb_comm.cu)
     int slab_fused = 1;
     int64_t rowblock_panel = 4096;
@@ -156,7 +156,15 @@ struct FftPass {
     // pointer into GPU d's symmetric window, NVLink load/store) instead of base + d * bs.
     int peer_out, peer_in;
     float2* peer[kMaxPeers];
+    // FB_FFT_TRACE builds only (tools/fft_trace.py): per-CTA timeline of the persistent pass,
+    // 32 u64 per CTA at trace + (trace_slot * 1024 + blockIdx) * 32 (null: off)
+    unsigned long long* trace;
+    int trace_slot;
 };
+#ifndef FB_FFT_TRACE
+#define FB_FFT_TRACE 0
+#endif
+extern unsigned long long* g_fft_trace_host;  // set by fb_debug_fft_trace (trace builds)
 fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t s);
 
 // Full single-GPU 2D FFT on device buffers (used by the API and the host/slab variants).

@@ -22,9 +22,12 @@ FB_FFT_EXTERN_L(0) FB_FFT_EXTERN_L(1) FB_FFT_EXTERN_L(2) FB_FFT_EXTERN_L(3) FB_F
 FB_FFT_EXTERN_L(5) FB_FFT_EXTERN_L(6) FB_FFT_EXTERN_L(7) FB_FFT_EXTERN_L(8) FB_FFT_EXTERN_L(9)
 FB_FFT_EXTERN_L(10) FB_FFT_EXTERN_L(11) FB_FFT_EXTERN_L(12) FB_FFT_EXTERN_L(13) FB_FFT_EXTERN_L(14)
 
+unsigned long long* g_fft_trace_host = nullptr;
+
 fb_status launch_fft_pass(const FftPass& p_in, const DeviceState* st, cudaStream_t s) {
     if (p_in.nlines <= 0) return FB_OK;
     FftPass p = p_in;
+    p.trace = FB_FFT_TRACE ? g_fft_trace_host : nullptr;
     const Knobs& kn = knobs();
     p.debug = kn.fft_debug;  // 0 unless built with FB_DEBUG_BUILD
     p.stagger_ns = kn.fft_stagger_ns;
@@ -179,6 +182,7 @@ fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inve
         p.scale = 1.f;
         p.col_like = 0;
         p.pair_log2N = ilog2(n0);
+        p.trace_slot = 0;
         FB_TRY(launch_fft_pass(p, st, s));
         // pass 2: for k_a in {0, 1}: length-n0/2 column FFTs over rows n0/2 k_a + n_b,
         // output X[k_a + 2 k_b] at row k_a + 2 k_b
@@ -194,6 +198,7 @@ fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inve
         p3.conj_out = inverse;
         p3.scale = scale;
         p3.col_like = 1;
+        p3.trace_slot = 1;
         return launch_fft_pass(p3, st, s);
     }
     const bool four_step = ilog2(n0) > max_onchip_col();
@@ -223,3 +228,10 @@ fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inve
 }
 
 }  // namespace fb
+
+#if FB_FFT_TRACE
+extern "C" int fb_debug_fft_trace(void* buf) {  // trace builds only: device buffer or null
+    fb::g_fft_trace_host = (unsigned long long*)buf;
+    return 0;
+}
+#endif

@@ -211,6 +211,18 @@ struct StageTw {
     }
 };
 
+// Barrier of the threads that share one exchange buffer: the whole CTA (id 0, __syncthreads)
+// or one sub-CTA of a multi-group persistent CTA (named barrier `id` over `n` threads).
+struct Sync {
+    int id, n;
+    __device__ __forceinline__ void operator()() const {
+        if (id == 0)
+            __syncthreads();
+        else
+            asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+    }
+};
+
 // Stage `S` (0-based): radix R, Ns = 16^S.  v[m] holds element t + m T of the stage input
 // on entry (stage 0: loaded by the caller) and of the stage output on exit.  `tw` holds this
 // stage's twiddles, prefetched by the previous stage just before its barrier (the element
@@ -221,7 +233,8 @@ template <int LOG2L, int C, int S, int STOP = 64>
 struct Stages {
     using G = LineGeom<LOG2L>;
     __device__ __forceinline__ static void run(float2* v, float2* sm, int t, int c,
-                                               const float2* __restrict__ stw, const float2* tw) {
+                                               const float2* __restrict__ stw, const float2* tw,
+                                               Sync sy = Sync{0, 0}) {
         if constexpr (S < G::NSTAGES && S != STOP) {
             constexpr int R = stage_radix(LOG2L, S);
             constexpr int Ns = 1 << (4 * S);
@@ -258,7 +271,7 @@ struct Stages {
             }
             if constexpr (!last) {
                 static_assert(Q == 1 && R == 16, "only the last stage may be a tail stage");
-                if constexpr (!first) __syncthreads();  // everyone has read the buffer
+                if constexpr (!first) sy();  // everyone has read the buffer
                 // write y[(t / Ns) Ns R + (t mod Ns) + r Ns]
                 if constexpr (Ns == 1) {
                     float2* wp = sm + (17 * t) * C + c;
@@ -272,8 +285,8 @@ struct Stages {
                 }
                 float2 twn[StageTw<LOG2L, S + 1>::NT];
                 if constexpr (S + 1 != STOP) StageTw<LOG2L, S + 1>::load(twn, t, stw);
-                __syncthreads();
-                Stages<LOG2L, C, S + 1, STOP>::run(v, sm, t, c, stw, twn);
+                sy();
+                Stages<LOG2L, C, S + 1, STOP>::run(v, sm, t, c, stw, twn, sy);
             }
         }
     }
@@ -373,7 +386,7 @@ struct ColPairLast {
     static constexpr int Q = G::E / R;
     static constexpr bool ok = (G::NSTAGES >= 2) && (Q % 2 == 0) && (C % 2 == 0);
     __device__ __forceinline__ static void run(float2* X, int t, int c, const float2* __restrict__ stw,
-                                               int conj_out, float scale) {
+                                               int conj_out, float scale, Sync sy = Sync{0, 0}) {
         if constexpr (ok) {
             constexpr int T = G::T, L = G::L, QH = Q / 2;
             const int cp = c & ~1;  // first column of the pair
@@ -388,7 +401,7 @@ struct ColPairLast {
                     b1[qq][r] = make_float2(x01.z, x01.w);
                 }
             }
-            __syncthreads();  // every thread has read its last-stage inputs; X becomes the output staging
+            sy();  // every thread has read its last-stage inputs; X becomes the output staging
 #pragma unroll
             for (int qq = 0; qq < QH; ++qq) {
                 const int j = 2 * t + (c & 1) + qq * 2 * T;
@@ -662,8 +675,15 @@ constexpr int tma_nb() {
     return (C * LineGeom<LOG2L>::T <= 256 && 3 * (TmaGeom<LOG2L, C, KIND, 1>::SMEM + 1024) <= 228 * 1024) ? 1 : 2;
 }
 
-template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB>
-__global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<LOG2L>::T>())
+// SUB > 1: one CTA per SM made of SUB independent sub-CTAs (C*T threads each, own staging and
+// exchange buffers, own mbarriers, named barrier 1 + sub), which take the CTA's groups
+// {blockIdx + i gridDim} from a shared-memory counter as they free up.  With SUB separate CTAs
+// per SM instead, each CTA had a fixed share and the warp arbiter starves some of them: in
+// the 2048^2 trace (tools/fft_trace.py) an SM's three CTAs finished 3-4 us apart and the last
+// one ran alone; the SM-local queue hands the remaining groups to whichever sub-CTA is free.
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB, int SUB = 1>
+__global__ void __launch_bounds__(SUB * C * LineGeom<LOG2L>::T,
+                                  SUB == 1 ? tma_minb<C * LineGeom<LOG2L>::T>() : 1)
     fft_pass_tma_kernel(const FftPass p, const __grid_constant__ CUtensorMap tin,
                         const __grid_constant__ CUtensorMap tout, const float2* __restrict__ tw,
                         const float2* __restrict__ stw, int64_t ngroups, int64_t nh_in) {
@@ -671,11 +691,16 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
     using TG = TmaGeom<LOG2L, C, KIND, NB>;
     static_assert(NB == 1 || NB == 2, "one or two staging buffers");
     constexpr int L = G::L, T = G::T, E = G::E;
+    constexpr int NT = C * T;  // threads of one (sub-)CTA
     extern __shared__ __align__(128) float2 smf[];
-    float2* Sbuf = smf;
-    float2* X = smf + NB * TG::S_ELEMS;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(X + TG::X_ELEMS);
-    const int tid = threadIdx.x;
+    const int sub = (SUB == 1) ? 0 : (int)(threadIdx.x / NT);
+    float2* Sbuf = smf + sub * (NB * TG::S_ELEMS + TG::X_ELEMS);
+    float2* X = Sbuf + NB * TG::S_ELEMS;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smf + SUB * (NB * TG::S_ELEMS + TG::X_ELEMS)) + 2 * sub;
+    __shared__ int64_t slot_grp[SUB][2];  // SUB > 1: group staged in buffer b of sub-CTA sub
+    __shared__ unsigned int q_next;        // SUB > 1: next index into this CTA's group list
+    const Sync sy{SUB == 1 ? 0 : 1 + sub, NT};
+    const int tid = (int)threadIdx.x - sub * NT;
     const int c = tid % C;
     const int t = tid / C;
     const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
@@ -685,14 +710,32 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
         ptx::mbar_init(ptx::smem_u32(&bars[0]), 1);
         ptx::mbar_init(ptx::smem_u32(&bars[1]), 1);
         ptx::fence_mbar_init();
-        if constexpr (KIND == KIND_COL) {
-            ptx::tma_prefetch_desc(&tin);
-            ptx::tma_prefetch_desc(&tout);
+        if (sub == 0) {
+            q_next = 0;
+            if constexpr (KIND == KIND_COL) {
+                ptx::tma_prefetch_desc(&tin);
+                ptx::tma_prefetch_desc(&tout);
+            }
         }
     }
     __syncthreads();
     ptx::pdl_launch_dependents();
     ptx::pdl_wait();  // PDL: everything above overlapped the previous grid's tail
+#if FB_FFT_TRACE
+    unsigned long long* tr =
+        p.trace ? p.trace + ((size_t)p.trace_slot * 1024 + blockIdx.x * SUB + sub) * 32 : nullptr;
+    auto gtime = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    };
+    if (tid == 0 && tr) {
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        tr[0] = smid;
+        tr[1] = gtime();
+    }
+#endif
 
     // thread 0: start the asynchronous fill of staging buffer `buf` with group `grp`
     auto issue = [&](int64_t grp, int buf) {
@@ -724,26 +767,52 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
 
     const int dbg = FB_DEBUG_BUILD ? p.debug : 0;  // timing decomposition (debug builds only)
     const bool dbg_noload = (dbg & 2) != 0;
-    if (tid == 0 && !dbg_noload) {
-        // Staggered start: CTA slot s (the s-th CTA placed on an SM) issues its first load
-        // s * stagger_ns later, so the slot-0 CTAs get their first group from a less crowded
-        // memory system and start computing earlier (interleaved A/B at 2048^2, 4 x 150 reps:
-        // 38.74 -> 38.21 us at 300 ns; no effect at 1024^2 / 4096^2).  Knob FB_FFT_STAGGER (ns);
-        // default 600 since the fused pair stage (3 x 200 reps interleaved, 2048^2: 300 ns 36.20,
-        // 600 ns 35.87, 900 ns 35.86, 1200 ns 35.95 us; 1024^2 / 4096^2 within 0.05 us).
+    // SUB > 1: thread 0 of a sub-CTA takes the next group of this CTA's list from q_next and
+    // publishes it in slot_grp before the buffer's mbarrier phase completes (the arrive has
+    // release semantics); "no more work" completes the phase with a plain arrive.
+    volatile int64_t* vslot = slot_grp[sub];
+    auto take = [&]() -> int64_t {
+        const int64_t g = blockIdx.x + (int64_t)atomicAdd(&q_next, 1u) * gridDim.x;
+        if constexpr (C % 2 == 0) {  // the pair twiddle is read right after the wait: warm it
+            if (p.pair_log2N > 0 && g < ngroups) {
+                const int64_t gq = (g * C) >> ((gshift >= 62) ? 62 : gshift);
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(tw + ((gq << (kTwLog2 - p.pair_log2N)) & (kTwN - 1))));
+            }
+        }
+        return g;
+    };
+    auto feed = [&](int64_t grp, int buf) {
+        vslot[buf] = grp;
+        if (grp < ngroups && !dbg_noload)
+            issue(grp, buf);
+        else
+            ptx::mbar_arrive(ptx::smem_u32(&bars[buf]));
+    };
+    if (tid == 0) {
+        // Staggered start: CTA slot s (the s-th CTA placed on an SM, or sub-CTA s) issues its
+        // first load s * stagger_ns later, so the slot-0 CTAs get their first group from a less
+        // crowded memory system and start computing earlier (interleaved A/B at 2048^2, 4 x 150
+        // reps: 38.74 -> 38.21 us at 300 ns; no effect at 1024^2 / 4096^2).  Knob FB_FFT_STAGGER
+        // (ns); default 600 since the fused pair stage (3 x 200 reps interleaved, 2048^2: 300 ns
+        // 36.20, 600 ns 35.87, 900 ns 35.86, 1200 ns 35.95 us; 1024^2 / 4096^2 within 0.05 us).
         if (p.stagger_ns > 0 && p.sm_count > 0) {
-            const int slot = (int)(blockIdx.x / (unsigned)p.sm_count);
+            const int slot = (SUB > 1) ? sub : (int)(blockIdx.x / (unsigned)p.sm_count);
             for (int i = 0; i < slot; ++i) __nanosleep((unsigned)p.stagger_ns);
         }
-        if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
-        if (NB == 2 && (int64_t)blockIdx.x + gridDim.x < ngroups) issue((int64_t)blockIdx.x + gridDim.x, 1);
+        if constexpr (SUB > 1) {
+            feed(take(), 0);
+            if (NB == 2) feed(take(), 1);
+        } else if (!dbg_noload) {
+            if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x, 0);
+            if (NB == 2 && (int64_t)blockIdx.x + gridDim.x < ngroups) issue((int64_t)blockIdx.x + gridDim.x, 1);
+        }
     }
     (void)nh_in;
 
     int it = 0;
-    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+    for (int64_t grp = blockIdx.x; SUB > 1 || grp < ngroups; grp += gridDim.x, ++it) {
         float2 wpair = make_float2(1.f, 0.f);  // pair-plan twiddle, loaded before the data wait
-        if constexpr (C % 2 == 0) {
+        if constexpr (C % 2 == 0 && SUB == 1) {
             if (p.pair_log2N > 0) {
                 const int64_t gq = (grp * C + c) >> ((gshift >= 62) ? 62 : gshift);
                 wpair = pair_twiddle(gq, p.pair_log2N, tw);
@@ -751,7 +820,24 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
         }
         const int buf = (NB == 2) ? (it & 1) : 0;
         const float2* S = Sbuf + buf * TG::S_ELEMS;
-        if (!dbg_noload) ptx::mbar_wait(ptx::smem_u32(&bars[buf]), (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u);
+#if FB_FFT_TRACE
+        if (tid == 0 && tr && it < 14) tr[2 + 2 * it] = gtime();
+#endif
+        if (SUB > 1 || !dbg_noload)
+            ptx::mbar_wait(ptx::smem_u32(&bars[buf]), (uint32_t)((NB == 2) ? (it >> 1) : it) & 1u);
+#if FB_FFT_TRACE
+        if (tid == 0 && tr && it < 14) tr[3 + 2 * it] = gtime();
+#endif
+        if constexpr (SUB > 1) {
+            grp = vslot[buf];
+            if (grp >= ngroups) break;  // uniform across the sub-CTA
+            if constexpr (C % 2 == 0) {
+                if (p.pair_log2N > 0) {
+                    const int64_t gq = (grp * C + c) >> ((gshift >= 62) ? 62 : gshift);
+                    wpair = pair_twiddle(gq, p.pair_log2N, tw);
+                }
+            }
+        }
         float2 v[E];
         if constexpr (KIND == KIND_COL) {
             const float2* sp = S + t * C + c;
@@ -772,16 +858,20 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
         if constexpr (KIND == KIND_COL) {
             if (tid == 0) ptx::bulk_wait_read0();  // previous group's TMA store has read X
         }
-        __syncthreads();  // S[buf] consumed by everyone; X free
-        if (tid == 0 && !dbg_noload) {
-            const int64_t nxt = grp + NB * (int64_t)gridDim.x;
-            if (nxt < ngroups) issue(nxt, buf);
+        sy();  // S[buf] consumed by everyone; X free
+        if (tid == 0) {
+            if constexpr (SUB > 1) {
+                feed(take(), buf);
+            } else if (!dbg_noload) {
+                const int64_t nxt = grp + NB * (int64_t)gridDim.x;
+                if (nxt < ngroups) issue(nxt, buf);
+            }
         }
 
         if constexpr (KIND == KIND_ROW && C == 2 && !OUT_GENERIC && PairLast<LOG2L>::ok) {
             if (p.pair_log2N > 0 && p.pair_half_shfl == 2 && p.tw4_log2N == 0 && !p.conj_out && p.scale == 1.0f &&
                 !dbg) {
-                Stages<LOG2L, C, 0, PairLast<LOG2L>::S>::run(v, X, t, c, stw, nullptr);
+                Stages<LOG2L, C, 0, PairLast<LOG2L>::S>::run(v, X, t, c, stw, nullptr, sy);
                 const int64_t gq = (grp * C) >> ((gshift >= 62) ? 62 : gshift);
                 float2* row0 = p.out + gq * p.lout.hi;
                 PairLast<LOG2L>::run(X, t, c, stw, wpair, row0, row0 + p.lout.lo);
@@ -790,10 +880,10 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
         }
         if constexpr (KIND == KIND_COL && ColPairLast<LOG2L, C>::ok) {
             if (p.col_pair_last && !p.col_stg && p.tw4_log2N == 0 && p.pair_log2N == 0 && !dbg) {
-                Stages<LOG2L, C, 0, ColPairLast<LOG2L, C>::S>::run(v, X, t, c, stw, nullptr);
-                ColPairLast<LOG2L, C>::run(X, t, c, stw, p.conj_out, p.scale);
+                Stages<LOG2L, C, 0, ColPairLast<LOG2L, C>::S>::run(v, X, t, c, stw, nullptr, sy);
+                ColPairLast<LOG2L, C>::run(X, t, c, stw, p.conj_out, p.scale, sy);
                 ptx::fence_proxy_async_smem();
-                __syncthreads();
+                sy();
                 if (tid == 0) {
                     const int64_t g0 = grp * C;
                     const int64_t gh0 = (gshift >= 62) ? 0 : (g0 >> gshift);
@@ -806,7 +896,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
                 continue;
             }
         }
-        if (!(dbg & 1)) Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr);
+        if (!(dbg & 1)) Stages<LOG2L, C, 0>::run(v, X, t, c, stw, nullptr, sy);
         if (dbg & 4) continue;
 
         const int64_t g = grp * C + c;
@@ -863,12 +953,12 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
 #pragma unroll
             for (int m = 0; m < E; ++m) dp[m * step] = v[m];
         } else if constexpr (KIND == KIND_COL) {
-            __syncthreads();  // last stage finished reading X
+            sy();  // last stage finished reading X
             float2* xp = X + t * C + c;
 #pragma unroll
             for (int m = 0; m < E; ++m) xp[m * T * C] = v[m];
             ptx::fence_proxy_async_smem();
-            __syncthreads();
+            sy();
             if (tid == 0) {
                 const int64_t g0 = grp * C;
                 const int64_t gh0 = (gshift >= 62) ? 0 : (g0 >> gshift);
@@ -904,6 +994,12 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T, tma_minb<C * LineGeom<
     if constexpr (KIND == KIND_COL) {
         if (tid == 0) ptx::bulk_wait0();
     }
+#if FB_FFT_TRACE
+    if (tid == 0 && tr) {
+        tr[30] = gtime();
+        tr[31] = it;
+    }
+#endif
 }
 
 // ------------------------------------------------------------ host side of the TMA path
@@ -938,18 +1034,19 @@ static bool make_col_map(CUtensorMap* m, const void* base, int64_t glo, int64_t 
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB = 2>
+template <int LOG2L, int C, int KIND, bool OUT_GENERIC, int NB = 2, int SUB = 1>
 static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     using TG = TmaGeom<LOG2L, C, KIND, NB>;
-    constexpr int threads = C * LineGeom<LOG2L>::T;
-    auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC, NB>;
+    constexpr int threads = SUB * C * LineGeom<LOG2L>::T;
+    constexpr size_t SMEM = (size_t)SUB * (NB * TG::S_ELEMS + TG::X_ELEMS) * sizeof(float2) + 64;
+    auto kern = fft_pass_tma_kernel<LOG2L, C, KIND, OUT_GENERIC, NB, SUB>;
     static DevOnce once;
     static std::atomic<int> occ[32];
     const int dev = DevOnce::dev();
     if (!once.done(dev)) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TG::SMEM));
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SMEM));
         int nb = 0;
-        FB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, TG::SMEM));
+        FB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, threads, SMEM));
         occ[dev].store(nb < 1 ? 1 : nb);
         once.set(dev);
     }
@@ -977,7 +1074,7 @@ static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStr
     // the TMA store).  Knob FB_FFT_COL_STG = 0 / 1 forces.
     FftPass pk = p;
     if (KIND == KIND_COL) pk.col_stg = (p.col_stg >= 0) ? p.col_stg : (C >= 16 ? 1 : 0);
-    FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), TG::SMEM, s, pk, tin, tout,
+    FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), SMEM, s, pk, tin, tout,
                       (const float2*)st->twiddles, (const float2*)st->stage_tw, ngroups, nh));
     return FB_OK;
 }
@@ -1044,6 +1141,15 @@ static fb_status launch_tma_nb(const FftPass& p, const DeviceState* st, cudaStre
     }
     if (knob_nb == 1 || knob_nb == 2) nb = knob_nb;
     if (nb == 3 - D) return launch_tma_one<LOG2L, C, KIND, false, 3 - D>(p, st, s);
+    if constexpr (D == 1 && (C * LineGeom<LOG2L>::T) % 32 == 0) {
+        // the one-buffer configuration runs as SUB = 3 sub-CTAs of one CTA per SM (SM-local
+        // group queue, see fft_pass_tma_kernel) when every sub-CTA streams many groups;
+        // knob FB_FFT_SUB=1: three separate CTAs always, 3: sub-CTAs always
+        const int64_t ngroups = (p.nlines + C - 1) / C;
+        const int sub = knobs().fft_sub;
+        if (sub == 3 || (sub == 0 && ngroups >= 48 * (int64_t)st->sm_count))
+            return launch_tma_one<LOG2L, C, KIND, false, 1, 3>(p, st, s);
+    }
     return launch_tma_one<LOG2L, C, KIND, false, D>(p, st, s);
 }
 
