@@ -46,6 +46,28 @@ def peaks():
             "source": "fallback (B200_PROFILING.md)"}
 
 
+def tc_peaks():
+    """tensor-core peaks measured on this pool's B200 by tools/peak_tc.cu
+    (profiles/r2_peaks.json): TF32 tcgen05 burst / sustained (data operands; the sustained run
+    sits at the 1 kW power cap) and FP64 DMMA.  One derivation for every GEMM roofline."""
+    p = os.path.join(ROOT, "profiles", "r2_peaks.json")
+    d = json.load(open(p))
+    return {"tf32_burst": float(d["tf32"]["use"]["burst"]), "tf32_sustained": float(d["tf32"]["use"]["sustained"]),
+            "f64": float(d["fp64_dmma"]["use"]),
+            "source": "measured: profiles/r2_peaks.json (tools/peak_tc.cu tcgen05 kind::tf32 / DMMA issue loops)"}
+
+
+def cpu_model() -> str:
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
 def ncu_traffic(kernel: str, workload: str):
     """dram bytes per launch from a committed `ncu --set full` summary, if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -185,7 +207,8 @@ def run_reference(args):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
             "scaling": "weak" if args.gpus > 1 else "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": "fft2d_2048x2048_fwd", "n0": n, "n1": n},
-            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": val, "unit": "GFLOP/s", "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu": cpu_model()},
             "e2e": {"value": val, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
     return 0
@@ -319,7 +342,7 @@ def main():
             tcpu = time.perf_counter() - t0
             err = oracle.rel_l2(y.cpu().numpy(), ref)
             out["cpu_baseline"] = {"value": fft_flops(n, n) / tcpu / 1e9, "unit": "GFLOP/s", "cores": thr,
-                                   "kind": "oracle", "seconds": tcpu,
+                                   "kind": "oracle", "seconds": tcpu, "cpu": cpu_model(),
                                    "sample": "the full 2048x2048 forward 2D DFT (naive O(n^2) per line, FP64) "
                                              "on the bench input, flops counted as 5 N log2 N"}
             out["parity"] = {"fft2d_2048_rel_l2_vs_oracle": err, "bar": 1e-5 * math.log2(n * n)}
@@ -367,7 +390,8 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                          args.warmup, flush, stream)
         tk = float(np.mean(mk))
         flops = 2.0 * n * n * n
-        tf32_peak = pk["bf16_tflops"] / 2.0  # TF32 dense = 1/2 of BF16 (guide's nominal ratio)
+        tcp = tc_peaks()
+        tf32_peak = tcp["tf32_burst"]  # measured tcgen05 kind::tf32 burst peak (K8)
         res["gemm_f32_2048"] = {
             "value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
             "config": {"workload": "gemm_2048^3_fp32_3xtf32", "configs_index": 2},
@@ -376,7 +400,8 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                          "frac": 3 * flops / (tk * 1e-3) / 1e12 / tf32_peak,
                          "note": "achieved counts the 3 TF32 MMAs (6MNK); useful 2MNK = achieved/3",
                          "traffic": ncu_traffic("gemm_3xtf32_kernel", "gemm_2048"),
-                         "peak_source": pk["source"] + " bf16 x 0.5 (TF32/BF16 nominal ratio)"}}
+                         "whole_call_frac": 3 * flops / (t * 1e-3) / 1e12 / tf32_peak,
+                         "peak_source": tcp["source"] + " -- TF32 burst, data operands"}}
         del A, B, C, ws, Ah, Al, Bh, Bl
     if want("gemm_f64_2048"):
         A = torch.from_numpy(synth.real_matrix(n, n, synth.TID_GEMM_A, dtype=np.float64)).cuda()
@@ -385,15 +410,13 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
         ms = timed_steps(torch, lambda: fb.fb_matmul(A, B, C, None, stream), steps, args.warmup, flush, stream)
         t = float(np.mean(ms))
         flops = 2.0 * n * n * n
-        # FP64 DMMA peak: ncu measured 26.8 TFLOP/s at 72.26 % tensor(DMMA)-pipe utilisation of the
-        # elapsed cycles (profiles/r1_gemm_f64_full.txt) -> 37.1 TFLOP/s at 100 % on this pool
-        f64_peak = pk.get("fp64_dmma_tflops", 37.1)
+        f64_peak = tc_peaks()["f64"]  # measured DMMA peak (K8)
         res["gemm_f64_2048"] = {
             "value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
             "config": {"workload": "gemm_2048^3_fp64_dmma", "configs_index": 2},
             "roofline": {"bound": "tensor", "kernel": "gemm_f64_dmma_kernel", "achieved": flops / (t * 1e-3) / 1e12,
                          "peak": f64_peak, "unit": "TFLOP/s", "frac": flops / (t * 1e-3) / 1e12 / f64_peak,
-                         "peak_source": "DMMA pipe peak derived from ncu utilisation (37.1 TFLOP/s)"}}
+                         "peak_source": tc_peaks()["source"] + " -- FP64 DMMA"}}
         del A, B, C
     # the paper's own matrix workload, LU of a 2048x2048 orthogonal matrix
     if want("lu_f64_2048"):
@@ -443,13 +466,15 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
         ws = torch.empty(fb.lib().fb_fft2d_workspace_bytes(m, m), dtype=torch.uint8, device="cuda")
         ms = timed_steps(torch, lambda: fb.fb_fft2d(x, y, ws, stream), steps, args.warmup, flush, stream)
         t = float(np.mean(ms))
-        passes = 3  # row pass + two four-step column passes
+        passes = 2  # the algorithmic traffic is 2 passes x (R + W) = 8 GiB at P = 1
         ach = passes * 2 * 8 * m * m / (t * 1e-3) / 1e9
         res["fft2d_16384"] = {"value": fft_flops(m, m) / (t * 1e-3) / 1e9, "unit": "GFLOP/s", "ms_per_step": t,
                               "config": {"workload": "fft2d_16384x16384_fwd_1gpu", "configs_index": 3},
                               "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                            "frac": ach / pk["hbm_gbs"],
-                                           "note": f"{passes} HBM passes x (R+W) of the 2 GiB array"}}
+                                           "note": "algorithmic 2 passes x (R+W) of the 2 GiB array = 8 GiB "
+                                                   "(SURVEY 8(d)); the implementation moves 3 passes (four-step "
+                                                   "16384-long columns)"}}
         del x, y, ws
     if want("gemm_bf16_8192"):  # N4: BF16 operands, FP32 accumulation (roofline: measured BF16 peak)
         n = 8192
@@ -493,7 +518,7 @@ def rowblock_gemm(args, torch, fb, np, stream, flush, pk, dist, rank, world, com
     t = max_over_ranks(torch, dist, float(np.mean(ms)))
     del A, B, C, ws
     flops = 2.0 * n * n * n
-    tf32_peak = pk["bf16_tflops_sustained"] / 2.0
+    tf32_peak = tc_peaks()["tf32_sustained"]
     return {"value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
             "config": {"workload": "gemm_32768^3_fp32_3xtf32_rowblock", "configs_index": 4,
                        "parallelism": f"rowblock{world}", "data": "uniform [-1, 1) (torch, seeded, on device)",
@@ -536,7 +561,7 @@ def run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, l
     gemm = rowblock_gemm(args, torch, fb, np, stream, flush, pk, dist, rank, world, comm)
     comm.destroy()
     val = fft_flops(n, n) / (t * 1e-3) / 1e9
-    hbm = 3 * 2 * 8 * n * n / world  # 3 local passes (row, 2 four-step column passes), R+W
+    hbm = 2 * 2 * 8 * n * n / world  # 2 local passes x (R+W) per GPU (8/4/2/1 GiB)
     ach = hbm / (t * 1e-3) / 1e9
     return {"value": val, "unit": "GFLOP/s", "ms_per_step": t, "scaling": "strong",
             "config": {"workload": "fft2d_16384x16384_slab", "n0": n, "n1": n, "configs_index": 3,
