@@ -44,6 +44,7 @@ static Knobs read_knobs() {
     k.fft_pair_tma = env_int("FB_FFT_PAIR_TMA", k.fft_pair_tma);
     k.fft_no_pdl = env_int("FB_FFT_NO_PDL", k.fft_no_pdl);
     k.fft_sub = env_int("FB_FFT_SUB", k.fft_sub);
+    k.fft_sub_ilv = env_int("FB_FFT_SUB_ILV", k.fft_sub_ilv);
     k.slab_fused = env_int("FB_SLAB_FUSED", k.slab_fused);
     const char* pk = getenv("FB_ROWBLOCK_PANEL");
     if (pk && pk[0]) k.rowblock_panel = atoll(pk);
@@ -52,6 +53,10 @@ static Knobs read_knobs() {
     k.gemm_splitv = env_int("FB_GEMM_SPLITV", k.gemm_splitv);
     k.gemm_split_pdl = env_int("FB_GEMM_SPLIT_PDL", k.gemm_split_pdl);
     k.gemm_1cta = env_int("FB_GEMM_1CTA", k.gemm_1cta);
+    k.gemm_fused = env_int("FB_GEMM_FUSED", k.gemm_fused);
+    k.gemm_lo_prepass = env_int("FB_GEMM_LO_PREPASS", k.gemm_lo_prepass);
+    k.gemm_streamk = env_int("FB_GEMM_STREAMK", k.gemm_streamk);
+
     k.bf16_cluster = env_int("FB_BF16_CLUSTER", k.bf16_cluster);
     k.lu_tma = env_int("FB_LU_TMA", k.lu_tma);
     k.lu_rank_simt = env_int("FB_LU_RANK_SIMT", k.lu_rank_simt);

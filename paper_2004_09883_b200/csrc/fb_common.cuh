@@ -62,11 +62,13 @@ struct Knobs {
     int fft_4step_lb = -1, fft_pair = 1, fft_pair_max_log2 = 11, fft_no_tma_col = 0, fft_col_c = 0;
     int fft_no_tma_row = 0, fft_col_nb = 0, fft_row_nb = 0, fft_no_tma = 0, fft_longrow = 1, fft_pair_tma = 1;
     int fft_no_pdl = 0, fft_debug = 0, fft_sub = 0;  // FB_FFT_SUB: 0 auto, 1 / 3 forced
+    int fft_sub_ilv = 0;
     // multi-GPU (fb_comm.cu)
     int slab_fused = 1;
     int64_t rowblock_panel = 4096;
     // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
     int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
+    int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 1;
     // LU (fb_lu.cu)
     int lu_tma = 1, lu_debug = 0, lu_rank_simt = 1, lu_serial = 0, lu_lookahead = 1, lu_graph = 1;
 };
@@ -160,6 +162,7 @@ struct FftPass {
     // 32 u64 per CTA at trace + (trace_slot * 1024 + blockIdx) * 32 (null: off)
     unsigned long long* trace;
     int trace_slot;
+    int sub_ilv;  // persistent pass with sub-CTAs: warps interleaved across sub-CTAs (knob)
 };
 #ifndef FB_FFT_TRACE
 #define FB_FFT_TRACE 0
@@ -187,6 +190,10 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
 fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
                             float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s);
 // G2-G4: C = Ah*Bh^T + Ah*Bl^T + Al*Bh^T with K-major split operands (A: m x k, B^T: n x k)
+// G1-G4 fused: C = A B (row-major FP32 A [m][k], B [k][n]), no workspace (fb_gemm_fused.cu)
+size_t gemm_3xtf32_fused_ws_bytes(int64_t m, int64_t n, int64_t k);
+fb_status gemm_3xtf32_fused_device(int64_t m, int64_t n, int64_t k, const float* A, int64_t lda, const float* B,
+                                   int64_t ldb, float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t s);
 fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
                                       int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
                                       int64_t ldc, cudaStream_t s);

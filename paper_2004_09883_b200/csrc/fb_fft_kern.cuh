@@ -693,14 +693,19 @@ __global__ void __launch_bounds__(SUB * C * LineGeom<LOG2L>::T,
     constexpr int L = G::L, T = G::T, E = G::E;
     constexpr int NT = C * T;  // threads of one (sub-)CTA
     extern __shared__ __align__(128) float2 smf[];
-    const int sub = (SUB == 1) ? 0 : (int)(threadIdx.x / NT);
+    // sub-CTA of this warp: interleaved (warp w -> sub w % SUB) so that every sub-CTA holds warps
+    // of every scheduler-priority level (the arbiter favours high warp ids; contiguous warp
+    // ranges would let one sub-CTA starve the others), or contiguous (knob FB_FFT_SUB_ILV=0)
+    const int wid = (int)(threadIdx.x >> 5);
+    const int sub = (SUB == 1) ? 0 : (p.sub_ilv ? wid % SUB : wid / (NT / 32));
     float2* Sbuf = smf + sub * (NB * TG::S_ELEMS + TG::X_ELEMS);
     float2* X = Sbuf + NB * TG::S_ELEMS;
     uint64_t* bars = reinterpret_cast<uint64_t*>(smf + SUB * (NB * TG::S_ELEMS + TG::X_ELEMS)) + 2 * sub;
     __shared__ int64_t slot_grp[SUB][2];  // SUB > 1: group staged in buffer b of sub-CTA sub
     __shared__ unsigned int q_next;        // SUB > 1: next index into this CTA's group list
     const Sync sy{SUB == 1 ? 0 : 1 + sub, NT};
-    const int tid = (int)threadIdx.x - sub * NT;
+    const int tid = (SUB == 1) ? (int)threadIdx.x
+                               : (p.sub_ilv ? (wid / SUB) * 32 + (int)(threadIdx.x & 31) : (int)threadIdx.x - sub * NT);
     const int c = tid % C;
     const int t = tid / C;
     const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
@@ -1073,6 +1078,7 @@ static fb_status launch_tma_one(const FftPass& p, const DeviceState* st, cudaStr
     // (C = 4, 32-byte segments) 37.84 -> 40.13 us and 4096^2 157.7 -> 167.1 us, so those keep
     // the TMA store).  Knob FB_FFT_COL_STG = 0 / 1 forces.
     FftPass pk = p;
+    pk.sub_ilv = knobs().fft_sub_ilv;
     if (KIND == KIND_COL) pk.col_stg = (p.col_stg >= 0) ? p.col_stg : (C >= 16 ? 1 : 0);
     FB_TRY(launch_pdl(kern, dim3((unsigned)grid), dim3(threads), SMEM, s, pk, tin, tout,
                       (const float2*)st->twiddles, (const float2*)st->stage_tw, ngroups, nh));

@@ -809,7 +809,12 @@ fb_status gemm_f64_sub_device(int64_t m, int64_t n, int64_t k, const double* A, 
 size_t gemm_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
     if (dtype == FB_F64) return 0;
     const int64_t kp = tf32::kpad(k);
-    return (size_t)(2 * m * kp + 2 * n * kp) * sizeof(float);
+    const size_t split = (size_t)(2 * m * kp + 2 * n * kp) * sizeof(float);  // default path
+    if (!knobs().gemm_fused) return split;
+    // FB_GEMM_FUSED=1: lo operands + stream-K partial slots (with less, the fused kernel forms
+    // lo in shared memory and needs no workspace)
+    const size_t fused = gemm_3xtf32_fused_ws_bytes(m, n, k);
+    return split > fused ? split : fused;
 }
 
 fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
@@ -821,7 +826,11 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
         if (cfg == 2) return launch_f64<f64::Cfg<128, 64, 2, 2>>(m, n, k, A, lda, B, ldb, C, ldc, s);
         return launch_f64<f64::CfgSmall>(m, n, k, A, lda, B, ldb, C, ldc, s);
     }
-    // ---- FP32 via 3xTF32: split A (same orientation), split B transposed, then the MMA kernel
+    // ---- FP32 via 3xTF32: one fused kernel (raw operands, lo formed in shared memory,
+    // fb_gemm_fused.cu); knob FB_GEMM_FUSED=0: split pre-pass (A as is, B transposed) + MMA kernel
+    if (knobs().gemm_fused)
+        return gemm_3xtf32_fused_device(m, n, k, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, ws,
+                                        ws_bytes, s);
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) {
         set_error("dimension exceeds int32");
         return FB_ERR_UNSUPPORTED_SIZE;

@@ -270,6 +270,23 @@ def test_gemm_path_variants(fb, knobs, dt, monkeypatch):
     assert oracle.rel_l2(C.cpu().numpy(), oracle.matmul(A.cpu().numpy(), B.cpu().numpy())) < bar
 
 
+@pytest.mark.parametrize("knobs", [{"FB_GEMM_FUSED": "1"}, {"FB_GEMM_FUSED": "1", "FB_GEMM_STREAMK": "0"},
+                                   {"FB_GEMM_FUSED": "1", "FB_GEMM_LO_PREPASS": "0"}])
+@pytest.mark.parametrize("m,n,k", [(300, 260, 203), (2048, 2048, 2048), (2048, 2048, 512), (64, 1000, 8), (1, 1, 1)])
+def test_gemm_fused_kernel_vs_oracle(fb, knobs, m, n, k, monkeypatch):
+    """The single-kernel FP32 path (fb_gemm_fused.cu: raw operands as the truncated TF32 hi part,
+    lo from a streaming pre-pass or formed in shared memory, B consumed MN-major, stream-K over
+    all SM pairs with a deterministic fix-up) against the oracle, and bitwise run to run."""
+    for kk, v in knobs.items():
+        monkeypatch.setenv(kk, v)
+    A = synth.real_matrix(m, k, synth.TID_GEMM_A)
+    B = synth.real_matrix(k, n, synth.TID_GEMM_B)
+    C1 = _mm_padded(fb, A, B)
+    C2 = _mm_padded(fb, A, B)
+    assert np.array_equal(C1, C2)
+    assert oracle.rel_l2(C1, oracle.matmul(A, B)) < 1e-5
+
+
 @pytest.mark.parametrize("m,n,k,bt", [(256, 256, 64, True), (300, 200, 136, False), (512, 768, 1000, True),
                                       (2048, 2048, 2048, False), (40, 24, 8, True)])
 def test_gemm_bf16_vs_oracle(fb, m, n, k, bt):
