@@ -34,6 +34,7 @@ struct fb_comm {
     // row-block GEMM: panel broadcasts run on their own stream
     cudaStream_t cstream = nullptr;
     cudaEvent_t cev = nullptr;
+    cudaEvent_t ev_bcast[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};  // panel slots
     int* flag_dev = nullptr;  // one int for the collective agreements (agree_min)
 };
 
@@ -342,6 +343,10 @@ fb_status fb_comm_destroy(fb_comm* c) {
         c->win_buf = nullptr;
     }
     if (c->cev) cudaEventDestroy(c->cev);
+    for (int i = 0; i < 2; ++i) {
+        if (c->ev_bcast[i]) cudaEventDestroy(c->ev_bcast[i]);
+        if (c->ev_used[i]) cudaEventDestroy(c->ev_used[i]);
+    }
     if (c->flag_dev) cudaFree(c->flag_dev);
     if (c->cstream) cudaStreamDestroy(c->cstream);
     if (c->nccl && c->devcomm_ok) {
@@ -490,12 +495,47 @@ fb_status fb_fft2d_slab_model(int P, int inverse, void* x, void* y, int64_t n0, 
     return FB_OK;
 }
 
+}  // extern "C"
+
+namespace fb {
+// Row-block GEMM layout of the workspace: [A hi | A lo] (FP32 only) then two panel slots, each
+// [packed B panel k x w (root's send buffer)] + (FP32) [panel hi | panel lo] (w x kp, K-major).
+struct RowblockWs {
+    int64_t w, kp;
+    size_t a_split, slot_pack, slot_split, slot, total;
+};
+static RowblockWs rowblock_ws(int dtype, int64_t ml, int64_t n, int64_t k, int64_t panel) {
+    RowblockWs r;
+    const size_t es = dtype == FB_F64 ? 8 : 4;
+    r.w = (panel > 0 && panel < n) ? panel : n;
+    r.kp = (k + 3) / 4 * 4;
+    auto al = [](size_t b) { return (b + 255) & ~(size_t)255; };
+    r.a_split = dtype == FB_F32 ? al((size_t)2 * ml * r.kp * 4) : 0;
+    r.slot_pack = al((size_t)k * r.w * es);
+    r.slot_split = dtype == FB_F32 ? al((size_t)2 * r.w * r.kp * 4) : 0;
+    r.slot = r.slot_pack + r.slot_split;
+    const size_t dflt = gemm_ws_bytes(dtype, ml, n, k);  // one-panel fallback (fb_matmul)
+    r.total = r.a_split + 2 * r.slot;
+    if (r.total < dflt) r.total = dflt;
+    return r;
+}
+}  // namespace fb
+
+extern "C" {
+
 size_t fb_matmul_rowblock_workspace_bytes(int nranks, int dtype, int64_t m, int64_t n, int64_t k) {
     if (nranks < 1 || m <= 0 || n <= 0 || k <= 0 || m % nranks) return 0;
     if (dtype != FB_F32 && dtype != FB_F64) return 0;
-    return gemm_ws_bytes(dtype, m / nranks, n, k);
+    return rowblock_ws(dtype, m / nranks, n, k, knobs().rowblock_panel).total;
 }
 
+// B is broadcast in N-column panels on the communicator's stream; the
+// GEMM of panel j (C[:, panel j] = A B[:, panel j], full K) runs on the caller's stream as soon as
+// panel j has landed, while panel j+1 is on the wire.  The root packs each panel into a
+// workspace slot (two slots, reused once the panel's split / GEMM has consumed it); non-root
+// ranks receive panel j into their B buffer at element offset k * j0, so after the call B on a
+// non-root rank holds B panel by panel ([panel][k][w]).  Per element the arithmetic equals
+// fb_matmul's (same K order and promotion chunks), so the result is bitwise the same.
 fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_t k, const void* A_rows,
                              int64_t lda, void* B, int64_t ldb, int root, void* C_rows, int64_t ldc,
                              void* ws, size_t ws_bytes, void* stream) {
@@ -504,55 +544,75 @@ fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_
         set_error("communicator is null or destroyed");
         return FB_ERR_NOT_INITIALIZED;
     }
-    if (m <= 0 || n <= 0 || k <= 0 || m % c->size || root < 0 || root >= c->size) {
-        set_error("bad sizes (m %% P must be 0) or root");
+    if ((dtype != FB_F32 && dtype != FB_F64) || m <= 0 || n <= 0 || k <= 0 || m % c->size || root < 0 ||
+        root >= c->size) {
+        set_error("bad dtype, sizes (m %% P must be 0) or root");
         return FB_ERR_INVALID_VALUE;
     }
     if (!B || ldb != n) {
         set_error("B must be a dense k x n buffer (ldb == n) on every rank");
         return FB_ERR_INVALID_VALUE;
     }
+    const size_t es = dtype == FB_F64 ? 8 : 4;
     const ncclDataType_t t = dtype == FB_F64 ? ncclDouble : ncclFloat;
     cudaStream_t s = (cudaStream_t)stream;
     const int64_t ml = m / c->size;
-    const int64_t pk = knobs().rowblock_panel;  // K rows per broadcast panel (FP32 path)
-    if (dtype == FB_F32 && pk > 0 && pk < k) {
-        // B is broadcast in contiguous K-row panels on a communication stream;
-        // the operand split of A runs meanwhile, and each B panel is split (transposed to
-        // K-major hi/lo) as soon as its broadcast has landed, then the tensor-core GEMM runs.
-        const size_t need = gemm_ws_bytes(dtype, ml, n, k);
-        if (!ws || ws_bytes < need || !aligned16(ws) || !aligned16(A_rows) || !aligned16(B) || !aligned16(C_rows) ||
-            (lda * 4) % 16 || (ldc * 4) % 16 || (n * 4) % 16 || lda < k || ldc < n) {
-            set_error("row-block GEMM: operands / workspace (%zu bytes) invalid", need);
-            return FB_ERR_INVALID_VALUE;
-        }
-        DeviceState* st;
-        FB_TRY(ensure_device(nullptr, &st));
-        if (!c->cstream) {
-            FB_CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
-            FB_CUDA_TRY(cudaEventCreateWithFlags(&c->cev, cudaEventDisableTiming));
-        }
-        const int64_t kp = (k + 3) / 4 * 4;
-        float* Ah = (float*)ws;
-        float* Al = Ah + ml * kp;
-        float* Bh = Al + ml * kp;
-        float* Bl = Bh + n * kp;
-        FB_CUDA_TRY(cudaEventRecord(c->cev, s));  // the broadcasts start after everything before the call
-        FB_CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->cev, 0));
-        FB_TRY(tf32_split_device(0, ml, k, (const float*)A_rows, lda, Ah, Al, kp, st, s));
-        for (int64_t p0 = 0; p0 < k; p0 += pk) {
-            const int64_t rows = (k - p0) < pk ? (k - p0) : pk;
-            float* Bp = (float*)B + p0 * n;
-            FB_NCCL_TRY(ncclBroadcast(Bp, Bp, (size_t)rows * (size_t)n, t, root, c->nccl, c->cstream), c->nccl);
-            FB_CUDA_TRY(cudaEventRecord(c->cev, c->cstream));
-            FB_CUDA_TRY(cudaStreamWaitEvent(s, c->cev, 0));  // binds to this panel's record
-            FB_TRY(tf32_split_device(1, rows, n, Bp, n, Bh + p0, Bl + p0, kp, st, s));
-        }
-        return gemm_3xtf32_presplit_device(ml, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C_rows, ldc, s);
+    const RowblockWs L = rowblock_ws(dtype, ml, n, k, knobs().rowblock_panel);
+    if (!ws || ws_bytes < L.total || !aligned16(ws) || !aligned16(A_rows) || !aligned16(B) || !aligned16(C_rows) ||
+        (lda * es) % 16 || (ldc * es) % 16 || (n * es) % 16 || (L.w * es) % 16 || lda < k || ldc < n) {
+        set_error("row-block GEMM: operands / workspace (%zu bytes) invalid", L.total);
+        return FB_ERR_INVALID_VALUE;
     }
-    // B broadcast from root (in place on root) -- the only data exchange of the row-block GEMM
-    FB_NCCL_TRY(ncclBroadcast(B, B, (size_t)k * (size_t)n, t, root, c->nccl, s), c->nccl);
-    return fb_matmul(dtype, ml, n, k, A_rows, lda, B, ldb, C_rows, ldc, ws, ws_bytes, stream);
+    DeviceState* st;
+    FB_TRY(ensure_device(nullptr, &st));
+    if (L.w >= n) {  // one panel: plain broadcast + fb_matmul
+        FB_NCCL_TRY(ncclBroadcast(B, B, (size_t)k * (size_t)n, t, root, c->nccl, s), c->nccl);
+        return gemm_device(dtype, ml, n, k, A_rows, lda, B, ldb, C_rows, ldc, ws, ws_bytes, st, s);
+    }
+    if (!c->cstream) {
+        FB_CUDA_TRY(cudaStreamCreateWithFlags(&c->cstream, cudaStreamNonBlocking));
+        FB_CUDA_TRY(cudaEventCreateWithFlags(&c->cev, cudaEventDisableTiming));
+        for (int i = 0; i < 2; ++i) {
+            FB_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_bcast[i], cudaEventDisableTiming));
+            FB_CUDA_TRY(cudaEventCreateWithFlags(&c->ev_used[i], cudaEventDisableTiming));
+        }
+    }
+    char* w0 = (char*)ws;
+    float* Ah = (float*)w0;
+    float* Al = Ah + ml * L.kp;
+    auto slot_pack = [&](int i) { return w0 + L.a_split + i * L.slot; };
+    auto slot_split = [&](int i) { return (float*)(w0 + L.a_split + i * L.slot + L.slot_pack); };
+    const bool is_root = c->rank == root;
+    FB_CUDA_TRY(cudaEventRecord(c->cev, s));  // the panel traffic starts after everything before the call
+    FB_CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->cev, 0));
+    if (dtype == FB_F32) FB_TRY(tf32_split_device(0, ml, k, (const float*)A_rows, lda, Ah, Al, L.kp, st, s));
+    int j = 0;
+    for (int64_t j0 = 0; j0 < n; j0 += L.w, ++j) {
+        const int64_t w = (n - j0) < L.w ? (n - j0) : L.w;
+        const int sl = j & 1;
+        // panel j on the wire (communicator stream); the root's slot is free once panel j-2 was consumed
+        void* panel = is_root ? (void*)slot_pack(sl) : (void*)((char*)B + (size_t)k * j0 * es);
+        if (is_root) {
+            if (j >= 2) FB_CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->ev_used[sl], 0));
+            FB_CUDA_TRY(cudaMemcpy2DAsync(panel, (size_t)w * es, (const char*)B + (size_t)j0 * es, (size_t)n * es,
+                                          (size_t)w * es, (size_t)k, cudaMemcpyDeviceToDevice, c->cstream));
+        }
+        FB_NCCL_TRY(ncclBroadcast(panel, panel, (size_t)k * (size_t)w, t, root, c->nccl, c->cstream), c->nccl);
+        FB_CUDA_TRY(cudaEventRecord(c->ev_bcast[sl], c->cstream));
+        // GEMM of panel j (caller's stream) as soon as it has landed
+        FB_CUDA_TRY(cudaStreamWaitEvent(s, c->ev_bcast[sl], 0));
+        if (dtype == FB_F32) {
+            float* Bh = slot_split(sl);
+            float* Bl = Bh + w * L.kp;
+            FB_TRY(tf32_split_device(1, k, w, (const float*)panel, w, Bh, Bl, L.kp, st, s));
+            FB_CUDA_TRY(cudaEventRecord(c->ev_used[sl], s));
+            FB_TRY(gemm_3xtf32_presplit_device(ml, w, k, Ah, Al, L.kp, Bh, Bl, L.kp, (float*)C_rows + j0, ldc, s));
+        } else {
+            FB_TRY(gemm_device(FB_F64, ml, w, k, A_rows, lda, panel, w, (double*)C_rows + j0, ldc, nullptr, 0, st, s));
+            FB_CUDA_TRY(cudaEventRecord(c->ev_used[sl], s));
+        }
+    }
+    return FB_OK;
 }
 
 }  // extern "C"

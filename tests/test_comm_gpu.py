@@ -148,21 +148,27 @@ def test_fused_model_vs_oracle(env):
     assert oracle.rel_l2(_assemble(y, P, n0, n1).cpu().numpy(), oracle.dft2d(xh)) < 5e-7
 
 
-@pytest.mark.parametrize("panel", ["64", "100", "0"])
-def test_rowblock_panel_broadcast_world1(env, panel, monkeypatch):
-    """The FP32 row-block GEMM broadcasts B in K-row panels on its own stream and splits each
-    panel as it lands; the product is bitwise the plain fb_matmul product
-    (same split arithmetic, same tensor-core kernel), ragged last panel included."""
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("panel", ["64", "100", "0", "512"])
+def test_rowblock_panel_broadcast_world1(env, panel, dt, monkeypatch):
+    """The row-block GEMM broadcasts B in N-column panels on the communicator's stream and runs
+    the GEMM of panel j (full K) as soon as it lands, while panel j+1 is on the wire (SURVEY
+    8(a) G5); the root packs each panel into a reused workspace slot.  The product is bitwise the
+    plain fb_matmul product (same per-element arithmetic), ragged last panel included, and the
+    root's B is left unchanged."""
     fb, comm = env
     monkeypatch.setenv("FB_ROWBLOCK_PANEL", panel)
-    m, n, k = 256, 192, 300
-    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).cuda()
-    B = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).cuda()
-    C = torch.empty(m, n, device="cuda")
-    comm.fb_matmul_rowblock(A, B, C, root=0)
-    ref = fb.matmul(A, B)
+    m, n, k = 256, 1192, 300
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(dt).cuda()
+    B = torch.from_numpy(synth.real_matrix(k, n, synth.TID_GEMM_B)).to(dt).cuda()
+    B0 = B.clone()
+    C = torch.empty(m, n, dtype=dt, device="cuda")
+    for _ in range(2):  # the second call reuses the slots and events
+        comm.fb_matmul_rowblock(A, B, C, root=0)
+    ref = fb.matmul(A, B0)
     torch.cuda.synchronize()
     assert torch.equal(C, ref)
+    assert torch.equal(B, B0)
 
 
 def test_fused_model_config3_full_size(env):
