@@ -45,6 +45,7 @@ static Knobs read_knobs() {
     k.fft_no_pdl = env_int("FB_FFT_NO_PDL", k.fft_no_pdl);
     k.fft_sub = env_int("FB_FFT_SUB", k.fft_sub);
     k.fft_sub_ilv = env_int("FB_FFT_SUB_ILV", k.fft_sub_ilv);
+    k.fft_col32 = env_int("FB_FFT_COL32", k.fft_col32);
     k.slab_fused = env_int("FB_SLAB_FUSED", k.slab_fused);
     const char* pk = getenv("FB_ROWBLOCK_PANEL");
     if (pk && pk[0]) k.rowblock_panel = atoll(pk);

@@ -56,13 +56,24 @@ __device__ __forceinline__ float2 cmul_cs(float2 x, float c, float s) {
     return __ffma2_rn(make_float2(x.y, x.x), make_float2(s, -s), t);
 }
 
+// cos(j pi / 16) and sin(j pi / 16), j = 0..16, as RN FP32 constants (the radix-2..32 internal
+// twiddles; the values for R <= 16 are the same constants as before the table existed)
+__device__ __forceinline__ constexpr float cos16(int j) {
+    constexpr float c1 = 0.980785280403230449126182236134239037f, c2 = 0.923879532511286756128183189396788933f,
+                    c3 = 0.831469612302545237078788377617905756f, c4 = 0.707106781186547524400844362104849039f,
+                    c5 = 0.555570233019602224742830813948532874f, c6 = 0.382683432365089771728459984030398866f,
+                    c7 = 0.195090322016128267848284868477022240f;
+    return j == 0 ? 1.f : j == 1 ? c1 : j == 2 ? c2 : j == 3 ? c3 : j == 4 ? c4 : j == 5 ? c5 : j == 6 ? c6
+         : j == 7 ? c7 : j == 8 ? 0.f : j == 9 ? -c7 : j == 10 ? -c6 : j == 11 ? -c5 : j == 12 ? -c4
+         : j == 13 ? -c3 : j == 14 ? -c2 : j == 15 ? -c1 : -1.f;
+}
+__device__ __forceinline__ constexpr float sin16(int j) { return j <= 8 ? cos16(8 - j) : cos16(j - 8); }
+
 // Radix-2 combine of the DIT recursion with the compile-time twiddle W_R^K = exp(-2 pi i K/R):
 // v[K] = e + W o, v[K + R/2] = e - W o.  K = 0 and K = R/4 (-i) need no multiply.
 template <int K, int R>
 __device__ __forceinline__ void butterfly(float2* v, float2 e, float2 o) {
-    constexpr float kS = 0.707106781186547524400844362104849039f;   // cos(pi/4)
-    constexpr float kC1 = 0.923879532511286756128183189396788933f;  // cos(pi/8)
-    constexpr float kS1 = 0.382683432365089771728459984030398866f;  // sin(pi/8)
+    static_assert(R <= 32, "radix > 32 not supported");
     if constexpr (K == 0) {
         v[K] = cadd(e, o);
         v[K + R / 2] = csub(e, o);
@@ -70,15 +81,9 @@ __device__ __forceinline__ void butterfly(float2* v, float2 e, float2 o) {
         v[K] = cadd_mi(e, o);
         v[K + R / 2] = csub_mi(e, o);
     } else {
-        // theta = 2 pi K / R in (0, pi), K != R/4; cos/sin as RN FP32 constants
-        constexpr float c = (8 * K == R) ? kS : (8 * K == 3 * R) ? -kS
-                          : (16 * K == R) ? kC1 : (16 * K == 3 * R) ? kS1
-                          : (16 * K == 5 * R) ? -kS1 : -kC1;
-        constexpr float s = (8 * K == R || 8 * K == 3 * R) ? kS
-                          : (16 * K == R || 16 * K == 7 * R) ? kS1 : kC1;
-        static_assert(8 * K == R || 8 * K == 3 * R || 16 * K == R || 16 * K == 3 * R || 16 * K == 5 * R ||
-                          16 * K == 7 * R,
-                      "radix > 16 not supported");
+        // theta = 2 pi K / R = j pi / 16 in (0, pi), K != R/4
+        constexpr int j = 32 * K / R;
+        constexpr float c = cos16(j), s = sin16(j);
         const float2 t = cmul_cs(o, c, s);
         v[K] = cadd(e, t);
         v[K + R / 2] = csub(e, t);
@@ -1292,6 +1297,154 @@ static fb_status launch_longrow(const FftPass& p, const DeviceState* st, cudaStr
                       (const float2*)st->twiddles, (const float2*)st->stage_tw);
 }
 
+// =====================================================================================
+// Column pass of 1024-long lines with 32 elements per thread (radix 32 x 32, one exchange).
+// 1024 = 32 x 32 four-step inside the CTA: thread (w, l) of a 4-column group (C = 4, 128
+// threads) owns column c = l & 3 and residue t = 8 w + (l >> 2); stage 1 is the length-32 DFT
+// of x[t + 32 m] (m < 32) in registers, then y[t][k1] *= W_1024^{t k1}; one shared-memory
+// transpose later the same thread owns (c, k1 = t) and runs the length-32 DFT over t, which
+// yields X[k1 + 32 k2].  Compared with the radix-16 pass (16 x 16 x 4: two exchanges, three
+// stages) it moves each element through shared memory once instead of twice and has one
+// barrier per exchange less.  All shared-memory patterns are conflict-free: the staging read
+// S[(t + 32 m) 4 + c] and the output staging [k][c] are contiguous per warp, and the exchange
+// E[c][k1][t] uses a 33-element row pitch and a 1060-element column pitch.
+// =====================================================================================
+constexpr int kC32Cols = 4, kC32Threads = 128;
+constexpr int kC32EPitch = 32 * 33 + 4;  // float2 per column in the exchange buffer
+constexpr int kC32S = kC32Cols * 1024;  // staging (float2)
+constexpr int kC32E = kC32Cols * kC32EPitch;
+constexpr size_t kC32Smem = (size_t)(kC32S + kC32E) * sizeof(float2) + 64;
+
+// W_1024^{t k} for k = 1..31 from the bases W_1024^{t 2^i} (i < 5; master table, resolution 2^14)
+__device__ __forceinline__ void c32_twiddles(float2* full, int t, const float2* __restrict__ tw) {
+    float2 b[5];
+#pragma unroll
+    for (int i = 0; i < 5; ++i) b[i] = __ldg(tw + (((t << i) << 4) & (kTwN - 1)));
+    tw_expand<32>(full, b);
+}
+
+template <int UNUSED = 0>  // a template so that every translation unit may include the definition
+__global__ void __launch_bounds__(kC32Threads, 3)
+    fft_col1024_kernel(const FftPass p, const __grid_constant__ CUtensorMap tin, const __grid_constant__ CUtensorMap tout,
+                       const float2* __restrict__ tw, int64_t ngroups) {
+    constexpr int C = kC32Cols, L = 1024, BOX = 256;
+    extern __shared__ __align__(128) float2 smf[];
+    float2* S = smf;
+    float2* E = smf + kC32S;  // exchange, then the output staging [k][c] (4096 float2)
+    uint64_t* bar = reinterpret_cast<uint64_t*>(E + kC32E);
+    const int tid = threadIdx.x, w = tid >> 5, l = tid & 31;
+    const int c = l & 3, t = 8 * w + (l >> 2);
+    const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+    const int64_t gmask = (gshift >= 62) ? -1 : ((int64_t(1) << gshift) - 1);
+    if (tid == 0) {
+        ptx::mbar_init(ptx::smem_u32(bar), 1);
+        ptx::fence_mbar_init();
+        ptx::tma_prefetch_desc(&tin);
+        ptx::tma_prefetch_desc(&tout);
+    }
+    __syncthreads();
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    auto issue = [&](int64_t grp) {
+        const uint32_t b = ptx::smem_u32(bar);
+        ptx::mbar_arrive_expect_tx(b, (uint32_t)(C * L * sizeof(float2)));
+        const int64_t g0 = grp * C;
+        const int64_t gh = (gshift >= 62) ? 0 : (g0 >> gshift);
+        const int gl = (int)(g0 & gmask);
+#pragma unroll 1
+        for (int kb = 0; kb < L; kb += BOX) ptx::tma_load_3d(ptx::smem_u32(S + kb * C), &tin, b, gl, kb, (int)gh);
+    };
+    if (tid == 0) {
+        if (p.stagger_ns > 0 && p.sm_count > 0) {
+            const int slot = (int)(blockIdx.x / (unsigned)p.sm_count);
+            for (int i = 0; i < slot; ++i) __nanosleep((unsigned)p.stagger_ns);
+        }
+        if ((int64_t)blockIdx.x < ngroups) issue(blockIdx.x);
+    }
+    // this thread's four-step twiddles W_1024^{t k1}, fixed for every group
+    float2 twf[31];
+    c32_twiddles(twf, t, tw);
+    int it = 0;
+    for (int64_t grp = blockIdx.x; grp < ngroups; grp += gridDim.x, ++it) {
+        ptx::mbar_wait(ptx::smem_u32(bar), (uint32_t)it & 1u);
+        float2 v[32];
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v[m] = S[(t + 32 * m) * C + c];
+        if (p.conj_in) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m].y = -v[m].y;
+        }
+        ptx::fence_proxy_async_smem();          // generic reads of S before its TMA refill
+        if (tid == 0) ptx::bulk_wait_read0();   // the previous group's TMA store has read E
+        __syncthreads();
+        if (tid == 0 && grp + gridDim.x < ngroups) issue(grp + gridDim.x);
+        // stage 1: length-32 DFT over m, then the four-step twiddle
+        dft<32>(v);
+#pragma unroll
+        for (int k = 1; k < 32; ++k) v[k] = cmul(v[k], twf[k - 1]);
+        // transpose: E[c][k1][t]
+        float2* ew = E + c * kC32EPitch + t;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) ew[k * 33] = v[k];
+        __syncthreads();
+        // stage 2: this thread owns (c, k1 = t): length-32 DFT over the residues t'
+        const float2* er = E + c * kC32EPitch + t * 33;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v[m] = er[m];
+        dft<32>(v);
+        if (p.conj_out) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m].y = -v[m].y;
+        }
+        if (p.scale != 1.0f) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = __fmul2_rn(v[m], bc2(p.scale));
+        }
+        __syncthreads();  // every thread has read its exchange row: E becomes the output staging
+        // X[k1 + 32 k2] -> staging [k][c]
+#pragma unroll
+        for (int m = 0; m < 32; ++m) E[(t + 32 * m) * C + c] = v[m];
+        ptx::fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+            const int64_t g0 = grp * C;
+            const int64_t gh0 = (gshift >= 62) ? 0 : (g0 >> gshift);
+            const int gl0 = (int)(g0 & gmask);
+#pragma unroll 1
+            for (int kb = 0; kb < L; kb += BOX) ptx::tma_store_3d(&tout, ptx::smem_u32(E + kb * C), gl0, kb, (int)gh0);
+            ptx::bulk_commit();
+        }
+    }
+    if (tid == 0) ptx::bulk_wait0();
+}
+
+static fb_status launch_col1024(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    static DevOnce once;
+    static std::atomic<int> occ[32];
+    const int dev = DevOnce::dev();
+    if (!once.done(dev)) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(fft_col1024_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kC32Smem));
+        int nb = 0;
+        FB_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, fft_col1024_kernel<0>, kC32Threads, kC32Smem));
+        occ[dev].store(nb < 1 ? 1 : nb);
+        once.set(dev);
+    }
+    const int64_t ngroups = (p.nlines + kC32Cols - 1) / kC32Cols;
+    int64_t grid = (int64_t)st->sm_count * occ[dev].load();
+    if (grid > ngroups) grid = ngroups;
+    const int gshift = p.g_shift >= 62 ? 62 : p.g_shift;
+    const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
+    const int64_t nh = (p.nlines + glo - 1) / glo;
+    CUtensorMap tin, tout;
+    if (!make_col_map(&tin, p.in, glo, 1024, nh, p.lin.es, p.lin.hi, kC32Cols) ||
+        !make_col_map(&tout, p.out, glo, 1024, nh, p.lout.es, p.lout.hi, kC32Cols)) {
+        set_error("cuTensorMapEncodeTiled failed for the radix-32 column pass");
+        return FB_ERR_CUDA;
+    }
+    return launch_pdl(fft_col1024_kernel<0>, dim3((unsigned)grid), dim3(kC32Threads), kC32Smem, s, p, tin, tout,
+                      (const float2*)st->twiddles, ngroups);
+}
+
 // All launches of one line length (explicitly instantiated per length in fb_fft_k*.cu so the
 // kernel variants compile in parallel translation units).
 template <int LOG2L>
@@ -1314,7 +1467,16 @@ fb_status launch_pass_L(const FftPass& p, const DeviceState* st, cudaStream_t s)
         return FB_ERR_UNSUPPORTED_SIZE;
     }
     if constexpr (has_tma) {
-        if (!g_fft_tma_disabled() && tma_eligible(p, kind, tc, og)) return launch_tma_L<LOG2L>(p, kind, tc, og, st, s);
+        if (!g_fft_tma_disabled() && tma_eligible(p, kind, tc, og)) {
+            if constexpr (LOG2L == 10) {
+                // 1024-long column lines in 4-column groups: the radix-32 one-exchange pass
+                // (knob FB_FFT_COL32=0: the radix-16 persistent pass)
+                if (kind == KIND_COL && tc == 4 && p.tw4_log2N == 0 && p.pair_log2N == 0 && knobs().fft_col32 &&
+                    !(p.col_stg > 0))
+                    return launch_col1024(p, st, s);
+            }
+            return launch_tma_L<LOG2L>(p, kind, tc, og, st, s);
+        }
     }
     if constexpr (LOG2L == 14) {
         if (longrow_eligible(p))

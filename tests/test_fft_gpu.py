@@ -346,6 +346,7 @@ def test_store_path_and_stagger_bitwise(fb, n0, n1, monkeypatch):
     arithmetic: results are bit-identical (forward and inverse)."""
     xh = synth.complex_field(n0, n1)
     x = torch.from_numpy(xh).cuda()
+    monkeypatch.setenv("FB_FFT_COL32", "0")  # these knobs select paths of the radix-16 pass
     outs = []
     for knobs in ({}, {"FB_FFT_COL_STG": "0"}, {"FB_FFT_COL_STG": "1"}, {"FB_FFT_STAGGER": "0"},
                   {"FB_FFT_PAIR2": "0"}, {"FB_FFT_PAIR2": "1"}, {"FB_FFT_PAIR2": "2"},
@@ -358,6 +359,31 @@ def test_store_path_and_stagger_bitwise(fb, n0, n1, monkeypatch):
         outs.append(np.concatenate([y.cpu().numpy(), fb.ifft2d(y).cpu().numpy()]))
     for o in outs[1:]:
         assert np.array_equal(o.view(np.uint32), outs[0].view(np.uint32))
+
+
+@pytest.mark.parametrize("n0,n1", [(2048, 2048), (2048, 1024), (2048, 256), (2048, 64)])
+def test_radix32_column_pass_vs_oracle(fb, n0, n1, monkeypatch):
+    """The 1024-long column pass of the pair plan (2048-row arrays) in its radix-32 one-exchange
+    form (fft_col1024_kernel) and in the radix-16 form (FB_FFT_COL32=0): both match the oracle
+    within the 5e-7 gate, forward and inverse (conj + exact 1/(n0 n1) scale in its epilogue),
+    and the radix-32 form is bitwise deterministic and in-place safe."""
+    xh = synth.complex_field(n0, n1)
+    ref = oracle.dft2d(xh)
+    x = torch.from_numpy(xh).cuda()
+    outs = {}
+    for v in ("1", "0"):
+        monkeypatch.setenv("FB_FFT_COL32", v)
+        y = fb.fft2d(x)
+        z = fb.ifft2d(y)
+        y2 = fb.fft2d(x)
+        xi = x.clone()
+        fb.fft2d(xi, out=xi)
+        torch.cuda.synchronize()
+        assert torch.equal(y, y2) and torch.equal(y, xi)
+        assert oracle.rel_l2(y.cpu().numpy(), ref) < 5e-7, v
+        assert oracle.rel_l2(z.cpu().numpy(), xh) < 5e-7, v
+        outs[v] = y.cpu().numpy()
+    assert oracle.rel_l2(outs["1"], outs["0"]) < 5e-7
 
 
 def test_longrow_kernel_matches_plain_kernel(fb, monkeypatch):
