@@ -276,15 +276,17 @@ def main():
         launches = (fb.launch_count() - L0) // (args.steps + args.warmup)
         t = float(np.mean(ms))
         gflops = fft_flops(n, n) / (t * 1e-3) / 1e9
-        # dominant kernel: fft_pass_kernel (2 launches per step: row pass, column pass); each
-        # launch reads and writes the 32 MiB array once -> 64 MiB algorithmic bytes per launch.
+        # the FFT pass kernels (2 launches per step: the radix-16 pair row pass
+        # fft_pass_tma_kernel and the radix-32 column pass fft_col1024_kernel); each launch reads
+        # and writes the 32 MiB array once -> 64 MiB algorithmic bytes per launch.
         bytes_launch = 2 * 8 * n * n
         achieved = bytes_launch / ((t / launches) * 1e-3) / 1e9
         out.update({"value": gflops, "unit": "GFLOP/s", "ms_per_step": t, "scaling": "strong",
                     "config": {"workload": "fft2d_2048x2048_fwd", "n0": n, "n1": n, "element": "complex64",
                                "l2": "flushed before every timed step (untimed): 512 MiB memset + 1 GiB read",
                                "configs_index": 1},
-                    "roofline": {"bound": "hbm", "kernel": "fft_pass_kernel (row pass + column pass)",
+                    "roofline": {"bound": "hbm",
+                                 "kernel": "fft_pass_tma_kernel (row pass) + fft_col1024_kernel (column pass)",
                                  "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                  "frac": achieved / pk["hbm_gbs"],
                                  "traffic": ncu_traffic("fft_pass_kernel", "fft2d_2048"),

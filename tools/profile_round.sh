@@ -7,7 +7,7 @@ timeout 600 $CMD > gpurun_out/prof_plain.json 2> gpurun_out/prof_plain.err || ex
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${R}_launches.csv $CMD > /dev/null 2>&1
 HCMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-extras"
 timeout 600 $HCMD > /dev/null 2>&1 || exit 1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fft_pass" -s 10 -c 2 -o gpurun_out/${R}_fft2048 $HCMD > gpurun_out/${R}_fft2048.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"fft_pass|fft_col1024" -s 10 -c 2 -o gpurun_out/${R}_fft2048 $HCMD > gpurun_out/${R}_fft2048.log 2>&1
 GCMD="python bench.py --steps 2 --warmup 3 --no-cpu-baseline --only gemm_f32_2048,gemm_f64_2048,lu_f64_2048"
 timeout 600 $GCMD > /dev/null 2>&1 || exit 1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm_3xtf32|split_both" -s 2 -c 2 -o gpurun_out/${R}_gemm $GCMD > gpurun_out/${R}_gemm.log 2>&1
