@@ -184,9 +184,9 @@ static fb_status check_fft_dims(int64_t n0, int64_t n1) {
         set_error("n0=%lld n1=%lld must be >= 1", (long long)n0, (long long)n1);
         return FB_ERR_INVALID_VALUE;
     }
-    if (!is_pow2(n0) || !is_pow2(n1) || n0 > kTwN || n1 > kTwN) {
-        set_error("FFT sizes must be powers of two in [1, %d] (got %lld x %lld)", kTwN,
-                  (long long)n0, (long long)n1);
+    if (!fft_size_ok(n0) || !fft_size_ok(n1)) {
+        set_error("FFT sizes must be powers of two in [1, %d] or other lengths in [1, 8192] (got %lld x %lld)",
+                  kTwN, (long long)n0, (long long)n1);
         return FB_ERR_UNSUPPORTED_SIZE;
     }
     return FB_OK;
@@ -565,6 +565,10 @@ fb_status fb_nr_fourn(float data[], const unsigned long nn[], int ndim, int isig
     const int64_t n0 = ndim == 2 ? (int64_t)nn[1] : 1;
     const int64_t n1 = ndim == 2 ? (int64_t)nn[2] : (int64_t)nn[1];
     FB_TRY(check_fft_dims(n0, n1));
+    if (!is_pow2(n0) || !is_pow2(n1)) {  // NR fourn's contract: every nn[i] a power of two
+        set_error("fourn: every nn[i] must be a power of two (got %lld x %lld)", (long long)n0, (long long)n1);
+        return FB_ERR_UNSUPPORTED_SIZE;
+    }
     DeviceState* st;
     int dev = 0;
     FB_TRY(ensure_device(&dev, &st));

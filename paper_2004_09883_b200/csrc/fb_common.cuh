@@ -174,6 +174,12 @@ fb_status launch_fft_pass(const FftPass& p, const DeviceState* st, cudaStream_t 
 size_t fft2d_ws_bytes(int64_t n0, int64_t n1);
 fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
                        size_t ws_bytes, const DeviceState* st, cudaStream_t s, bool unscaled = false);
+// Non-power-of-two sizes (fb_bluestein.cu): each dimension a power of two <= 16384 or any
+// length <= 8192 (Bluestein chirp-z over power-of-two passes)
+bool fft_size_ok(int64_t n);
+size_t bluestein_ws_bytes(int64_t n0, int64_t n1);
+fb_status fft2d_bluestein(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws, size_t ws_bytes,
+                          const DeviceState* st, cudaStream_t s, bool unscaled);
 // Column transform of an n0 x ncols block with leading dimension ld (in place allowed when
 // n0 <= 4096); used by 2D and slab paths.
 fb_status fft_columns(const float2* in, float2* out, int64_t n0, int64_t ncols, int64_t ld_in,

@@ -155,12 +155,14 @@ static bool use_pair_plan(int64_t n0, int64_t n1) {
 }
 
 size_t fft2d_ws_bytes(int64_t n0, int64_t n1) {
+    if (!is_pow2(n0) || !is_pow2(n1)) return bluestein_ws_bytes(n0, n1);
     if (ilog2(n0) <= max_onchip_col() && !use_pair_plan(n0, n1)) return 0;
     return (size_t)n0 * (size_t)n1 * sizeof(float2);
 }
 
 fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws,
                        size_t ws_bytes, const DeviceState* st, cudaStream_t s, bool unscaled) {
+    if (!is_pow2(n0) || !is_pow2(n1)) return fft2d_bluestein(x, y, n0, n1, inverse, ws, ws_bytes, st, s, unscaled);
     const float scale = (inverse && !unscaled) ? 1.0f / (float)((double)n0 * (double)n1) : 1.0f;
     if (use_pair_plan(n0, n1) && aligned16(x) && aligned16(y) && aligned16(ws)) {
         if (ws_bytes < fft2d_ws_bytes(n0, n1)) {

@@ -41,10 +41,14 @@ def test_status_strings_and_version(L):
 
 def test_fft_validation_without_device(L):
     p = ctypes.c_void_p(16)
-    # not a power of two -> FB_ERR_UNSUPPORTED_SIZE (2), nothing enqueued
-    assert L.fb_fft2d(p, p, 3, 4, None, 0, None) == 2
+    # beyond 16384 (power of two) or 8192 (other lengths) -> FB_ERR_UNSUPPORTED_SIZE (2)
+    assert L.fb_fft2d(p, p, 8193, 4, None, 0, None) == 2
     assert L.fb_fft2d(p, p, 32768, 4, None, 0, None) == 2
     assert b"power" in L.fb_last_error_detail()
+    # other lengths <= 8192 (Bluestein) are accepted and need a workspace (FB_ERR_WORKSPACE, 4)
+    assert L.fb_fft2d(p, p, 3, 4, None, 0, None) == 4
+    assert L.fb_fft2d_workspace_bytes(3, 4) > 0 and L.fb_fft2d_workspace_bytes(8191, 8192) > 0
+    assert L.fb_fft2d_workspace_bytes(8193, 8) == 0
     assert L.fb_fft2d(p, p, 0, 4, None, 0, None) == 1
     assert L.fb_fft2d(None, p, 4, 4, None, 0, None) == 1
     # misaligned
@@ -60,7 +64,7 @@ def test_fft_validation_without_device(L):
     one = L.fb_fft2d_host_workspace_bytes(2048, 2048)
     assert L.fb_fft2d_host_batch_workspace_bytes(2048, 2048) == 2 * ((one + 255) // 256 * 256)
     assert L.fb_fft2d_host_batch(p, p, 2048, 2048, 0, 0, p, 1 << 40, None) == 1
-    assert L.fb_fft2d_host_batch(p, p, 2048, 3000, 2, 0, p, 1 << 40, None) == 2
+    assert L.fb_fft2d_host_batch(p, p, 2048, 10000, 2, 0, p, 1 << 40, None) == 2
     assert L.fb_fft2d_host_batch(p, p, 2048, 2048, 2, 0, p, one, None) == 4
 
 

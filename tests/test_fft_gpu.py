@@ -386,6 +386,43 @@ def test_radix32_column_pass_vs_oracle(fb, n0, n1, monkeypatch):
     assert oracle.rel_l2(outs["1"], outs["0"]) < 5e-7
 
 
+@pytest.mark.parametrize("n0,n1", [(3, 5), (7, 64), (1, 999), (1000, 1), (100, 36), (360, 480), (12, 8191),
+                                   (2048, 1000), (625, 243)])
+def test_non_power_of_two_vs_oracle(fb, n0, n1):
+    """sizes that are not powers of two (Bluestein chirp-z over the power-of-two
+    passes, fb_bluestein.cu) against the full oracle, forward and inverse, within the north_star
+    bar 1e-5 log2(n0 n1); in place equals out of place."""
+    x = synth.complex_field(n0, n1, tensor_id=7)
+    ref = oracle.dft2d(x)
+    y = _run(fb, x)
+    e = oracle.rel_l2(y, ref)
+    z = _run(fb, y, inverse=True)
+    ei = oracle.rel_l2(z, oracle.dft2d(y, inverse=True))
+    print(f"{n0}x{n1}: forward {e:.2e} inverse {ei:.2e}")
+    assert e < _bar(n0, n1) and ei < _bar(n0, n1), (e, ei)
+    assert e < 2e-6  # the measured level (FP32 chirp-z): well inside the bar
+    assert np.array_equal(_run(fb, x, inplace=True), y)
+
+
+def test_non_power_of_two_closed_forms(fb):
+    """Tone and delta closed forms at a non-power-of-two size (3 * 5 * 7 * 11 x 2 * 3^4)."""
+    n0, n1 = 1155, 162
+    f0, f1 = 77, 13
+    i0 = np.arange(n0)[:, None]
+    i1 = np.arange(n1)[None, :]
+    tone = np.exp(2j * np.pi * (((f0 * i0) % n0) / n0 + ((f1 * i1) % n1) / n1)).astype(np.complex64)
+    yt = _run(fb, tone)
+    assert abs(yt[f0, f1] - n0 * n1) < 1e-4 * n0 * n1
+    yt[f0, f1] = 0
+    assert np.abs(yt).max() < 1e-4 * n0 * n1
+    d = np.zeros((n0, n1), np.complex64)
+    a, b = 401, 99
+    d[a, b] = 1
+    yd = _run(fb, d)
+    ref = np.exp(-2j * np.pi * (((i0 * a) % n0) / n0 + ((i1 * b) % n1) / n1))
+    assert np.abs(yd - ref).max() < 1e-5
+
+
 def test_longrow_kernel_matches_plain_kernel(fb, monkeypatch):
     """16384-long rows: the persistent half-prefetching kernel and the plain kernel run the same
     per-line arithmetic (bit for bit), and both match the oracle on sampled rows."""
