@@ -57,6 +57,7 @@ static Knobs read_knobs() {
     k.gemm_fused = env_int("FB_GEMM_FUSED", k.gemm_fused);
     k.gemm_lo_prepass = env_int("FB_GEMM_LO_PREPASS", k.gemm_lo_prepass);
     k.gemm_streamk = env_int("FB_GEMM_STREAMK", k.gemm_streamk);
+    k.gemm_lo_overlap = env_int("FB_GEMM_LO_OVERLAP", k.gemm_lo_overlap);
 
     k.bf16_cluster = env_int("FB_BF16_CLUSTER", k.bf16_cluster);
     k.lu_tma = env_int("FB_LU_TMA", k.lu_tma);

@@ -68,7 +68,7 @@ struct Knobs {
     int64_t rowblock_panel = 4096;
     // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
     int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
-    int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 1;
+    int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 0, gemm_lo_overlap = 0;
     // LU (fb_lu.cu)
     int lu_tma = 1, lu_debug = 0, lu_rank_simt = 1, lu_serial = 0, lu_lookahead = 1, lu_graph = 1;
 };

@@ -35,6 +35,7 @@ namespace fb {
 namespace fused {
 
 constexpr int BK = 32, STAGES = 3;
+constexpr int LO_PANEL_KB = 8;  // lo pre-pass panel: 8 k-blocks = 256 k, one completion flag each
 constexpr int NUM_CONV_WARPS = 2, NUM_EPI_WARPS = 8;
 // PRE = false: lo formed in shared memory by converter warps 2-3 (epilogue warps 4-11);
 // PRE = true: lo tiles come from a streaming pre-pass in global memory (epilogue warps 2-9)
@@ -136,7 +137,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(num_threads<PRE>(), 
     gemm_3xtf32_fused_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                              const __grid_constant__ CUtensorMap tmAl, const __grid_constant__ CUtensorMap tmBl,
                              float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n,
-                             float* __restrict__ partials, unsigned int* __restrict__ flags) {
+                             float* __restrict__ partials, unsigned int* __restrict__ flags,
+                             const unsigned int* __restrict__ pflags, unsigned int pflag_target) {
     constexpr int EPI_WARP0 = epi_warp0<PRE>();
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_u32 = ptx::smem_u32(smem_raw);
@@ -191,12 +193,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(num_threads<PRE>(), 
     ptx::cluster_sync();
     ptx::tc_fence_after();
     const uint32_t tmem_base = *tmem_slot_ptr;
-    ptx::pdl_wait();  // PDL: A and B are complete (the setup above overlapped the previous kernel)
+    // PDL: A and B are complete (the setup above overlapped the previous kernel).  With panel
+    // flags (pflags) the kernel instead overlaps the lo pre-pass: the producer waits for each
+    // K panel's flag before loading from it (the pre-pass itself waited for the previous kernel).
+    if (!pflags) ptx::pdl_wait();
 
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer: this CTA's A rows and B columns, raw FP32
             int g = 0;  // k-blocks issued so far (stage ring position)
+            uint32_t panels_ready = 0;  // K panels (LO_PANEL_KB k-blocks each) seen complete
             for (int ip = 0; ip < npc; ++ip) {
             const Piece pc = get_piece(ip, pair, P, U, KB);
             int tm, tn;
@@ -207,6 +213,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(num_threads<PRE>(), 
                 const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
                 ptx::mbar_wait(empty_bar(s), ph ^ 1u);
                 const int kc = kb * BK;
+                if (pflags) {
+                    const uint32_t pnl = (uint32_t)(kb / LO_PANEL_KB);
+                    while (panels_ready <= pnl) {  // panels complete in order, mostly
+                        uint32_t v;
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(pflags + pnl) : "memory");
+                        if (v >= pflag_target) {
+                            panels_ready = pnl + 1;
+                            break;
+                        }
+                        __nanosleep(64);
+                    }
+                }
                 if constexpr (PRE) {
                     // all four tiles; both CTAs' bytes complete on the leader's full barrier
                     if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * STAGE_BYTES);
@@ -422,27 +440,105 @@ static fb_status make_map(CUtensorMap* map, const float* ptr, int64_t inner, int
 }  // namespace fused
 
 namespace fused {
-// lo pre-pass: lo[r][c] = lo_of(x[r][c]) for an rows x cols matrix (row pitches ldx, ldl in
-// elements, multiples of 4 by the API contract); float4 streaming, one read and one write.
-__global__ void __launch_bounds__(256) lo_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
-                                                 int64_t ldx, float* __restrict__ L, int64_t ldl,
-                                                 unsigned int* __restrict__ flags, int nflags) {
+// lo pre-pass, both operands in one launch: lo[r][c] = lo_of(x[r][c]) for A (m x k, pitches
+// lda -> kp) in blocks [0, nblk_a) and B (k x n, ldb -> np) in the rest; each thread moves
+// LO_UNROLL float4 per iteration with every load issued before the first store (memory-level
+// parallelism: one float4 per thread in flight left the pass latency-bound at ~4 TB/s).
+constexpr int LO_UNROLL = 4;
+__device__ __forceinline__ void lo_part(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
+                                        float* __restrict__ L, int64_t ldl, int64_t blk, int64_t nblk) {
+    const int64_t c4 = (cols + 3) / 4;
+    const int64_t total = rows * c4;
+    const int64_t stride = nblk * blockDim.x;
+    for (int64_t e0 = blk * blockDim.x + threadIdx.x; e0 < total; e0 += stride * LO_UNROLL) {
+        float4 v[LO_UNROLL];
+        int64_t r[LO_UNROLL], c[LO_UNROLL];
+#pragma unroll
+        for (int u = 0; u < LO_UNROLL; ++u) {
+            const int64_t e = e0 + u * stride;
+            r[u] = e / c4;
+            c[u] = (e - r[u] * c4) * 4;
+            if (e < total) v[u] = __ldcs(reinterpret_cast<const float4*>(X + r[u] * ldx + c[u]));
+        }
+#pragma unroll
+        for (int u = 0; u < LO_UNROLL; ++u)
+            if (e0 + u * stride < total)
+                *reinterpret_cast<float4*>(L + r[u] * ldl + c[u]) =
+                    make_float4(lo_of(v[u].x), lo_of(v[u].y), lo_of(v[u].z), lo_of(v[u].w));
+    }
+}
+// Panel-ordered lo pre-pass for the overlapped form: one block per SM (so that every block is
+// resident at once and the GEMM, launched when all of them have started, fits beside them),
+// walking the K panels in order; each block does its strided share of panel p
+// (A[:, panel] and B[panel, :]) and then counts itself in pflags[p] (target: gridDim.x).
+__global__ void __launch_bounds__(256) lo_panel_kernel(const float* __restrict__ A, int64_t m, int64_t k, int64_t lda,
+                                                       float* __restrict__ Al, int64_t kp, const float* __restrict__ B,
+                                                       int64_t n, int64_t ldb, float* __restrict__ Bl, int64_t np,
+                                                       int npanels, unsigned int* __restrict__ pflags) {
+    ptx::pdl_launch_dependents();  // the GEMM may start now; it waits on pflags instead
+    ptx::pdl_wait();               // A and B are complete
+    constexpr int PK = LO_PANEL_KB * BK;  // k per panel (multiple of 4)
+    const int64_t n4 = (n + 3) / 4;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int pnl = 0; pnl < npanels; ++pnl) {
+        const int64_t k0 = (int64_t)pnl * PK;
+        const int64_t kw = (k - k0) < PK ? (k - k0) : PK;
+        const int64_t a4 = (kw + 3) / 4;
+        const int64_t wa = m * a4, total = wa + kw * n4;
+        for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < total; e0 += stride * LO_UNROLL) {
+            float4 v[LO_UNROLL];
+            float* dst[LO_UNROLL];
+#pragma unroll
+            for (int u = 0; u < LO_UNROLL; ++u) {
+                const int64_t e = e0 + u * stride;
+                dst[u] = nullptr;
+                if (e < total) {
+                    const float* src;
+                    if (e < wa) {
+                        const int64_t r = e / a4, c = k0 + (e - r * a4) * 4;
+                        src = A + r * lda + c;
+                        dst[u] = Al + r * kp + c;
+                    } else {
+                        const int64_t eb = e - wa;
+                        const int64_t r = k0 + eb / n4, c = (eb % n4) * 4;
+                        src = B + r * ldb + c;
+                        dst[u] = Bl + r * np + c;
+                    }
+                    v[u] = __ldcs(reinterpret_cast<const float4*>(src));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < LO_UNROLL; ++u)
+                if (dst[u])
+                    *reinterpret_cast<float4*>(dst[u]) =
+                        make_float4(lo_of(v[u].x), lo_of(v[u].y), lo_of(v[u].z), lo_of(v[u].w));
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            atomicAdd(pflags + pnl, 1u);
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) lo_kernel(const float* __restrict__ A, int64_t m, int64_t k, int64_t lda,
+                                                 float* __restrict__ Al, int64_t kp, const float* __restrict__ B,
+                                                 int64_t n, int64_t ldb, float* __restrict__ Bl, int64_t np,
+                                                 int64_t nblk_a, unsigned int* __restrict__ flags, int nflags) {
     ptx::pdl_launch_dependents();
     ptx::pdl_wait();
     if (blockIdx.x == 0)  // the stream-K flags of the GEMM that follows start at zero
         for (int i = threadIdx.x; i < nflags; i += blockDim.x) flags[i] = 0u;
-    const int64_t c4 = (cols + 3) / 4;
-    const int64_t total = rows * c4;
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t r = e / c4, c = (e - r * c4) * 4;
-        const float4 x = *reinterpret_cast<const float4*>(X + r * ldx + c);
-        *reinterpret_cast<float4*>(L + r * ldl + c) = make_float4(lo_of(x.x), lo_of(x.y), lo_of(x.z), lo_of(x.w));
-    }
+    if ((int64_t)blockIdx.x < nblk_a)
+        lo_part(A, m, k, lda, Al, kp, blockIdx.x, nblk_a);
+    else
+        lo_part(B, k, n, ldb, Bl, np, blockIdx.x - nblk_a, gridDim.x - nblk_a);
 }
 template <bool PRE>
 static fb_status launch(const CUtensorMap& mA, const CUtensorMap& mB, const CUtensorMap& mAl, const CUtensorMap& mBl,
                         int64_t m, int64_t n, int64_t k, float* C, int64_t ldc, int pairs, float* partials,
-                        unsigned int* flags, cudaStream_t s) {
+                        unsigned int* flags, cudaStream_t s, const unsigned int* pflags = nullptr,
+                        unsigned int pflag_target = 0) {
     static DevOnce once;
     const int dev = DevOnce::dev();
     if (!once.done(dev)) {
@@ -468,7 +564,7 @@ static fb_status launch(const CUtensorMap& mA, const CUtensorMap& mB, const CUte
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, gemm_3xtf32_fused_kernel<PRE>, mA, mB, mAl, mBl, C, (int)m, (int)n, (int)k,
-                                   ldc, tiles_m, tiles_n, partials, flags));
+                                   ldc, tiles_m, tiles_n, partials, flags, pflags, pflag_target));
     FB_LAUNCH_CHECK("gemm_3xtf32_fused_kernel");
     return FB_OK;
 }
@@ -490,7 +586,8 @@ static FusedWs fused_ws_layout(int64_t m, int64_t n, int64_t k) {
     w.bl = ((size_t)(m * kp) * 4 + 255) & ~(size_t)255;
     w.part = w.bl + (((size_t)(k * np) * 4 + 255) & ~(size_t)255);
     w.flags = w.part + (size_t)pmax * 65536 * 4;
-    w.total = w.flags + (size_t)kMaxPairs * 4 + 256;
+    const int64_t npanels = ((k + fused::BK - 1) / fused::BK + fused::LO_PANEL_KB - 1) / fused::LO_PANEL_KB;
+    w.total = w.flags + (size_t)(kMaxPairs + npanels) * 4 + 256;
     return w;
 }
 size_t gemm_3xtf32_fused_ws_bytes(int64_t m, int64_t n, int64_t k) { return fused_ws_layout(m, n, k).total; }
@@ -526,15 +623,28 @@ fb_status gemm_3xtf32_fused_device(int64_t m, int64_t n, int64_t k, const float*
     if (pairs > sk_units(m, n, k)) pairs = sk_units(m, n, k);
     FB_TRY(fused::make_map(&mAl, Al, k, m, kp, 128u));
     FB_TRY(fused::make_map(&mBl, Bl, n, k, np, 32u, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B));
-    const int64_t work = m * (kp / 4) + k * (np / 4);
-    int64_t blocks = (work + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
-    const int64_t ba = blocks * (m * (kp / 4)) / (work > 0 ? work : 1);
-    // one launch per operand keeps the kernel simple; both stream at full bandwidth
-    fused::lo_kernel<<<(unsigned)(ba > 0 ? ba : 1), 256, 0, s>>>(A, m, k, lda, Al, kp, flags, kMaxPairs);
-    FB_LAUNCH_CHECK("lo_kernel(A)");
-    fused::lo_kernel<<<(unsigned)(blocks - ba > 0 ? blocks - ba : 1), 256, 0, s>>>(B, k, n, ldb, Bl, np, flags, 0);
-    FB_LAUNCH_CHECK("lo_kernel(B)");
+    if (knobs().gemm_lo_overlap) {
+        // the lo pre-pass in K panels, overlapped with the GEMM: the kernel's producer waits on
+        // each panel's flag (zeroed here together with the stream-K flags) instead of PDL-waiting
+        // for the whole pre-pass
+        const int64_t npanels = ((k + fused::BK - 1) / fused::BK + fused::LO_PANEL_KB - 1) / fused::LO_PANEL_KB;
+        unsigned int* pflags = flags + kMaxPairs;
+        FB_CUDA_TRY(cudaMemsetAsync(flags, 0, (size_t)(kMaxPairs + npanels) * 4, s));
+        const int grid = st->sm_count;  // one block per SM: all resident, beside the GEMM's CTAs
+        fused::lo_panel_kernel<<<grid, 256, 0, s>>>(A, m, k, lda, Al, kp, B, n, ldb, Bl, np, (int)npanels, pflags);
+        FB_LAUNCH_CHECK("lo_panel_kernel");
+        return fused::launch<true>(mA, mB, mAl, mBl, m, n, k, C, ldc, (int)pairs, partials, flags, s, pflags,
+                                   (unsigned int)grid);
+    }
+    const int64_t wa = m * (kp / 4), wb = k * (np / 4);
+    int64_t blocks = (wa + wb + 256 * fused::LO_UNROLL - 1) / (256 * fused::LO_UNROLL);
+    if (blocks > (int64_t)st->sm_count * 8) blocks = (int64_t)st->sm_count * 8;
+    if (blocks < 2) blocks = 2;
+    int64_t ba = (blocks * wa + (wa + wb) / 2) / (wa + wb);
+    if (ba < 1) ba = 1;
+    if (ba > blocks - 1) ba = blocks - 1;
+    fused::lo_kernel<<<(unsigned)blocks, 256, 0, s>>>(A, m, k, lda, Al, kp, B, n, ldb, Bl, np, ba, flags, kMaxPairs);
+    FB_LAUNCH_CHECK("lo_kernel");
     return fused::launch<true>(mA, mB, mAl, mBl, m, n, k, C, ldc, (int)pairs, partials, flags, s);
 }
 

@@ -270,7 +270,8 @@ def test_gemm_path_variants(fb, knobs, dt, monkeypatch):
     assert oracle.rel_l2(C.cpu().numpy(), oracle.matmul(A.cpu().numpy(), B.cpu().numpy())) < bar
 
 
-@pytest.mark.parametrize("knobs", [{"FB_GEMM_FUSED": "1"}, {"FB_GEMM_FUSED": "1", "FB_GEMM_STREAMK": "0"},
+@pytest.mark.parametrize("knobs", [{"FB_GEMM_FUSED": "1"}, {"FB_GEMM_FUSED": "1", "FB_GEMM_STREAMK": "1"},
+                                   {"FB_GEMM_FUSED": "1", "FB_GEMM_LO_OVERLAP": "1"},
                                    {"FB_GEMM_FUSED": "1", "FB_GEMM_LO_PREPASS": "0"}])
 @pytest.mark.parametrize("m,n,k", [(300, 260, 203), (2048, 2048, 2048), (2048, 2048, 512), (64, 1000, 8), (1, 1, 1)])
 def test_gemm_fused_kernel_vs_oracle(fb, knobs, m, n, k, monkeypatch):
