@@ -177,18 +177,23 @@ struct TwCount {
 // FB_FFT_TWREC, all of them).  r = hb + rest (hb = highest power of two <= r):
 // W^{jm r} = W^{jm rest} * W^{jm hb}.
 template <int R, int r = 1>
-__device__ __forceinline__ void tw_expand(float2* full, const float2* b) {
+__device__ __forceinline__ void pow_expand(float2* full, const float2* b) {  // always from bases
     if constexpr (r < R) {
-        if constexpr (FB_FFT_TWREC) {
-            constexpr int i = ilog2c(r), hb = 1 << i;
-            if constexpr (r == hb)
-                full[r - 1] = b[i];
-            else
-                full[r - 1] = cmul(full[r - hb - 1], b[i]);
-        } else {
-            full[r - 1] = b[r - 1];
-        }
-        tw_expand<R, r + 1>(full, b);
+        constexpr int i = ilog2c(r), hb = 1 << i;
+        if constexpr (r == hb)
+            full[r - 1] = b[i];
+        else
+            full[r - 1] = cmul(full[r - hb - 1], b[i]);
+        pow_expand<R, r + 1>(full, b);
+    }
+}
+template <int R>
+__device__ __forceinline__ void tw_expand(float2* full, const float2* b) {
+    if constexpr (FB_FFT_TWREC) {
+        pow_expand<R>(full, b);
+    } else {
+#pragma unroll
+        for (int r = 1; r < R; ++r) full[r - 1] = b[r - 1];
     }
 }
 // load this butterfly's stored twiddles from the [r][jm] table row base twp (= table + jm)
@@ -196,6 +201,37 @@ template <int R, int Ns>
 __device__ __forceinline__ void tw_load(float2* b, const float2* __restrict__ twp) {
 #pragma unroll
     for (int i = 0; i < TwCount<R>::value; ++i) b[i] = __ldg(twp + (FB_FFT_TWREC ? (1 << i) : (i + 1)) * Ns);
+}
+
+// Four-step twiddles W_N^{gh k} for this thread's elements k = t + m T (m < E), N = 2^log2N:
+// one scattered load a = W^{gh t} and log2(E) warp-uniform bases W^{gh T 2^i}; the powers
+// b^m = W^{gh T m} come from tw_expand, then v[m] *= a b^m (FB_FFT_TW4REC = 1, default).  With
+// FB_FFT_TW4REC = 0 every element loads its own twiddle (E scattered loads per thread; the
+// 16384^2 first four-step pass ran at 70 % of the copy bandwidth that way).
+#ifndef FB_FFT_TW4REC
+#define FB_FFT_TW4REC 1
+#endif
+template <int E, int T>
+__device__ __forceinline__ void apply_tw4(float2* v, int64_t gh, int t, int log2N, const float2* __restrict__ tw) {
+    const int64_t msk = (int64_t(1) << log2N) - 1;
+    const int sh = kTwLog2 - log2N;
+    if constexpr (FB_FFT_TW4REC && E >= 2) {
+        constexpr int LE = ilog2c(E);
+        const float2 a = __ldg(tw + (((gh * (int64_t)t) & msk) << sh));
+        float2 b[LE], full[E - 1];
+#pragma unroll
+        for (int i = 0; i < LE; ++i) b[i] = __ldg(tw + (((gh * (int64_t)(T << i)) & msk) << sh));
+        pow_expand<E>(full, b);
+        v[0] = cmul(v[0], a);
+#pragma unroll
+        for (int m = 1; m < E; ++m) v[m] = cmul(v[m], cmul(a, full[m - 1]));
+    } else {
+#pragma unroll
+        for (int m = 0; m < E; ++m) {
+            const int64_t e = (gh * (int64_t)(t + m * T)) & msk;
+            v[m] = cmul(v[m], __ldg(tw + (e << sh)));
+        }
+    }
 }
 
 template <int LOG2L, int S>
@@ -504,16 +540,7 @@ __global__ void __launch_bounds__(C * LineGeom<LOG2L>::T,
     }
 
     if (!valid) return;
-    if (p.tw4_log2N > 0) {
-        // four-step twiddle W_N^{gh k}, N = 2^tw4 (the master table has resolution 2^14)
-        const int tw4 = p.tw4_log2N;
-#pragma unroll
-        for (int m = 0; m < G::E; ++m) {
-            const int k = t + m * G::T;
-            const int64_t e = (gh * (int64_t)k) & ((int64_t(1) << tw4) - 1);
-            v[m] = cmul(v[m], __ldg(tw + (e << (kTwLog2 - tw4))));
-        }
-    }
+    if (p.tw4_log2N > 0) apply_tw4<G::E, G::T>(v, gh, t, p.tw4_log2N, tw);  // four-step twiddle W_N^{gh k}
     if (p.conj_out) {
 #pragma unroll
         for (int m = 0; m < G::E; ++m) v[m].y = -v[m].y;
@@ -938,15 +965,7 @@ __global__ void __launch_bounds__(SUB * C * LineGeom<LOG2L>::T,
         if constexpr (C % 2 == 0) {
             if (p.pair_log2N > 0) pair_radix2<E>(v, c & 1, wpair);
         }
-        if (p.tw4_log2N > 0) {
-            const int tw4 = p.tw4_log2N;
-#pragma unroll
-            for (int m = 0; m < E; ++m) {
-                const int k = t + m * T;
-                const int64_t e = (gh * (int64_t)k) & ((int64_t(1) << tw4) - 1);
-                v[m] = cmul(v[m], __ldg(tw + (e << (kTwLog2 - tw4))));
-            }
-        }
+        if (p.tw4_log2N > 0) apply_tw4<E, T>(v, gh, t, p.tw4_log2N, tw);  // four-step twiddle W_N^{gh k}
         if (p.conj_out) {
 #pragma unroll
             for (int m = 0; m < E; ++m) v[m].y = -v[m].y;
@@ -1105,9 +1124,12 @@ static bool tma_eligible(const FftPass& p, int& kind, int& C, bool& out_generic)
         if (knobs().fft_no_tma_col) return false;
         // widest row segment (up to 128 B = 16 columns) whose double-buffered staging plus
         // exchange buffer stays near 100 KiB (two CTAs per SM)
-        C = (l <= 8) ? 16 : (l == 9 ? 8 : (l == 10 ? 4 : 2));
+        // widest row segment whose staging stays small: 128-long columns (the 16384^2 four-step
+        // passes) take 32 columns = 256-byte segments (A/B 2721 -> 2534 us at 16384^2: the first
+        // four-step pass gathers rows 16 MiB apart, where longer DRAM bursts pay)
+        C = (l == 6 || l == 7) ? 32 : (l <= 8) ? 16 : (l == 9 ? 8 : (l == 10 ? 4 : 2));
         const int kc = knobs().fft_col_c;
-        if (kc == 2 || kc == 4 || kc == 8 || kc == 16) C = kc;
+        if (kc == 2 || kc == 4 || kc == 8 || kc == 16 || (kc == 32 && (l == 6 || l == 7))) C = kc;
         if (C * (1 << l) / 16 > 1024 || (size_t)C * (1 << l) * 8 * 3 > 200 * 1024) return false;
         const int64_t glo = (gshift >= 62) ? p.nlines : (int64_t(1) << gshift);
         if (glo % C) return false;
@@ -1174,6 +1196,8 @@ static fb_status launch_tma_L(const FftPass& p, int kind, int C, bool og, const 
             if (C == 8) return launch_tma_nb<LOG2L, 8, KIND_COL>(p, st, s, knobs().fft_col_nb);
         if constexpr (16 * T <= 1024 && LOG2L <= 10)
             if (C == 16) return launch_tma_nb<LOG2L, 16, KIND_COL>(p, st, s, knobs().fft_col_nb);
+        if constexpr (32 * T <= 256 && (LOG2L == 6 || LOG2L == 7))
+            if (C == 32) return launch_tma_nb<LOG2L, 32, KIND_COL>(p, st, s, knobs().fft_col_nb);
     } else {
         if (C == 2) return launch_tma_nb<LOG2L, 2, KIND_ROW>(p, st, s, knobs().fft_row_nb);
         if (!og) return launch_tma_nb<LOG2L, 1, KIND_ROW>(p, st, s, knobs().fft_row_nb);
@@ -1320,7 +1344,7 @@ __device__ __forceinline__ void c32_twiddles(float2* full, int t, const float2* 
     float2 b[5];
 #pragma unroll
     for (int i = 0; i < 5; ++i) b[i] = __ldg(tw + (((t << i) << 4) & (kTwN - 1)));
-    tw_expand<32>(full, b);
+    pow_expand<32>(full, b);
 }
 
 template <int UNUSED = 0>  // a template so that every translation unit may include the definition

@@ -9,7 +9,7 @@ IFS=';' read -ra SZ <<< "$SIZES"
 for r in $(seq $ROUNDS); do
   for sz in "${SZ[@]}"; do
     for v in "${VV[@]}"; do
-      env $v timeout 120 python tools/fft_pass_bench.py $sz 100 | sed "s/}}/}, \"variant\": \"$v\"}/" >> gpurun_out/ab_env.jsonl 2>&1
+      env $v timeout 120 python tools/fft_pass_bench.py $sz 100 | VAR="$v" python -c "import json,os,sys; d=json.loads(sys.stdin.read()); d['variant']=os.environ['VAR']; print(json.dumps(d))" >> gpurun_out/ab_env.jsonl 2>&1
     done
   done
 done
