@@ -1305,6 +1305,143 @@ static bool longrow_eligible(const FftPass& p) {
     return knobs().fft_longrow != 0 && !g_fft_tma_disabled();
 }
 
+// =====================================================================================
+// 16384-long rows as a 32 x 32 x 16 four-step inside one 512-thread CTA (one line at a time,
+// one CTA per SM), 32 elements per thread:
+//   A  thread t < 512: length-32 DFT of x[t + 512 m] (loaded straight from global memory: each
+//      warp load is 256 contiguous bytes; the next line was prefetched into L2 by one bulk
+//      prefetch), times W_16384^{t k1} -> E1[k1][t] (pitch 513: conflict-free both ways);
+//   B  thread (k1 = lane, t1 = warp): length-32 DFT over t2 of y[t1 + 16 t2][k1], times
+//      W_512^{t1 k2b} -> E2[k2b][t1][k1];
+//   C  thread (k1 = lane, warp w): for k2b in {2w, 2w+1} the length-16 DFT over t1 ->
+//      X[k1 + 32 k2b + 1024 k2c], stored as 256-byte warp segments.
+// Two shared-memory exchanges and three barriers per line, against four stages / three
+// exchanges and a half-line staging scheme in fft_longrow_kernel.
+// =====================================================================================
+// v[r] *= W^r (r = 1..31) from the bases b[i] = W^{2^i} (i < 5) with few live registers:
+// W^r = W^{4a} W^{b}, r = 4a + b, from the 3 low and 7 high powers (10 values, 5 products).
+__device__ __forceinline__ void apply_pow32(float2* v, const float2* b) {
+    float2 lo[4], hi[8];
+    lo[1] = b[0];
+    lo[2] = b[1];
+    lo[3] = cmul(b[0], b[1]);
+    hi[1] = b[2];
+    hi[2] = b[3];
+    hi[3] = cmul(b[2], b[3]);
+    hi[4] = b[4];
+    hi[5] = cmul(b[2], b[4]);
+    hi[6] = cmul(b[3], b[4]);
+    hi[7] = cmul(hi[3], b[4]);
+#pragma unroll
+    for (int r = 1; r < 32; ++r) {
+        const int a = r >> 2, bb = r & 3;
+        const float2 w = (a == 0) ? lo[bb] : (bb == 0) ? hi[a] : cmul(hi[a], lo[bb]);
+        v[r] = cmul(v[r], w);
+    }
+}
+
+constexpr int kL14Threads = 512;
+constexpr int kL14P1 = 513;
+constexpr size_t kL14Smem = (size_t)32 * kL14P1 * sizeof(float2) + 64;
+
+template <bool OUT_GENERIC>
+__global__ void __launch_bounds__(kL14Threads, 1)
+    fft_row16384_kernel(const FftPass p, const float2* __restrict__ tw) {
+    extern __shared__ __align__(128) float2 smf[];
+    float2* E = smf;
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    const int64_t nl = p.nlines;
+    int64_t g = blockIdx.x;
+    if (tid == 0 && g < nl)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.in + g * p.lin.hi), "r"(16384u * 8u)
+                     : "memory");
+    for (; g < nl; g += gridDim.x) {
+        const int64_t gn = g + gridDim.x;
+        if (tid == 0 && gn < nl)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.in + gn * p.lin.hi), "r"(16384u * 8u)
+                         : "memory");
+        float2 v[32];
+        {
+            const float2* src = p.in + g * p.lin.hi + tid;
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = __ldcs(src + 512 * m);
+        }
+        if (p.conj_in) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m].y = -v[m].y;
+        }
+        // ---- A
+        dft<32>(v);
+        {
+            float2 bA[5];  // W_16384^{tid 2^i} (reloaded per line: L1 hits, fewer live registers)
+#pragma unroll
+            for (int i = 0; i < 5; ++i) bA[i] = __ldg(tw + ((tid << i) & (kTwN - 1)));
+            apply_pow32(v, bA);
+        }
+        __syncthreads();  // the previous line's stage C has read E
+#pragma unroll
+        for (int k = 0; k < 32; ++k) E[k * kL14P1 + tid] = v[k];
+        __syncthreads();
+        // ---- B: (k1 = lane, t1 = w), values over t2
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v[m] = E[lane * kL14P1 + w + 16 * m];
+        dft<32>(v);
+        {
+            float2 bB[5];  // W_512^{w 2^i}
+#pragma unroll
+            for (int i = 0; i < 5; ++i) bB[i] = __ldg(tw + (((w << i) << 5) & (kTwN - 1)));
+            apply_pow32(v, bB);
+        }
+        __syncthreads();  // every thread has read E1
+#pragma unroll
+        for (int k = 0; k < 32; ++k) E[(k * 16 + w) * 32 + lane] = v[k];  // E2[k2b][t1][k1]
+        __syncthreads();
+        // ---- C: k2b in {2w, 2w + 1}, length-16 DFT over t1
+        float2* dst = p.out + g * p.lout.hi;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k2b = 2 * w + h;
+            float2 u[16];
+#pragma unroll
+            for (int t1 = 0; t1 < 16; ++t1) u[t1] = E[(k2b * 16 + t1) * 32 + lane];
+            dft<16>(u);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                float2 o = u[c];
+                if (p.conj_out) o.y = -o.y;
+                if (p.scale != 1.0f) o = __fmul2_rn(o, bc2(p.scale));
+                const int k = lane + 32 * k2b + 1024 * c;
+                if constexpr (!OUT_GENERIC) {
+                    dst[k] = o;
+                } else {  // per-peer column blocks (the slab transpose), as fft_longrow_kernel
+                    const int out_kmask = (1 << p.lout.kb_shift) - 1;
+                    if (p.peer_out)
+                        p.peer[k >> p.lout.kb_shift][g * p.lout.hi + (int64_t)(k & out_kmask) * p.lout.es] = o;
+                    else
+                        dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] = o;
+                }
+            }
+        }
+    }
+}
+
+template <bool OG>
+static fb_status launch_row16384(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    static DevOnce once;
+    const int dev = DevOnce::dev();
+    if (!once.done(dev)) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(fft_row16384_kernel<OG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kL14Smem));
+        once.set(dev);
+    }
+    int64_t grid = st->sm_count;
+    if (grid > p.nlines) grid = p.nlines;
+    return launch_pdl(fft_row16384_kernel<OG>, dim3((unsigned)grid), dim3(kL14Threads), kL14Smem, s, p,
+                      (const float2*)st->twiddles);
+}
+
 template <bool OG>
 static fb_status launch_longrow(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     using G = LineGeom<14>;
@@ -1503,8 +1640,14 @@ fb_status launch_pass_L(const FftPass& p, const DeviceState* st, cudaStream_t s)
         }
     }
     if constexpr (LOG2L == 14) {
-        if (longrow_eligible(p))
+        if (longrow_eligible(p)) {
+            // the 32 x 32 x 16 four-step kernel, plain or per-peer outputs (knob FB_FFT_ROW16K=0:
+            // the radix-16 half-line-streaming kernel)
+            if (knobs().fft_row16k)
+                return p.lout.kb_shift >= 14 && !p.peer_out ? launch_row16384<false>(p, st, s)
+                                                            : launch_row16384<true>(p, st, s);
             return p.lout.kb_shift >= 14 && !p.peer_out ? launch_longrow<false>(p, st, s) : launch_longrow<true>(p, st, s);
+        }
     }
     return launch_L<LOG2L>(p, pick_C(LOG2L, p.col_like != 0), st, s);
 }
