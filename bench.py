@@ -524,11 +524,13 @@ def rowblock_gemm(args, torch, fb, np, stream, flush, pk, dist, rank, world, com
     return {"value": flops / (t * 1e-3) / 1e12, "unit": "TFLOP/s", "ms_per_step": t,
             "config": {"workload": "gemm_32768^3_fp32_3xtf32_rowblock", "configs_index": 4,
                        "parallelism": f"rowblock{world}", "data": "uniform [-1, 1) (torch, seeded, on device)",
-                       "b_broadcast": "ncclBroadcast inside the timed region" if comm is not None else "none"},
+                       "b_broadcast": ("N-column panels (FB_ROWBLOCK_PANEL) broadcast inside the timed region, "
+                                       "each panel's GEMM overlapping the next panel's broadcast")
+                       if comm is not None else "none"},
             "roofline": {"bound": "tensor", "achieved": 3 * flops / world / (t * 1e-3) / 1e12, "peak": tf32_peak,
                          "unit": "TFLOP/s", "frac": 3 * flops / world / (t * 1e-3) / 1e12 / tf32_peak,
                          "note": "per GPU, counting the 3 TF32 MMAs (6MNK/P), split pre-pass and broadcast "
-                                 "inside the time; peak = sustained BF16 x 0.5"}}
+                                 "inside the time; peak = measured sustained TF32 (profiles/r2_peaks.json)"}}
 
 
 def run_slab(args, torch, fb, synth, np, stream, flush, pk, dist, rank, world, local):
