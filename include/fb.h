@@ -124,7 +124,8 @@ size_t fb_matmul_workspace_bytes(int dtype, int64_t m, int64_t n, int64_t k);
 
 /* BF16 GEMM: C[m][n] (float32) = A[m][k] * op(B), A and B bfloat16 (raw
  * 16-bit storage), exact BF16 products accumulated in FP32 on tcgen05 (kind::f16, CTA pairs),
- * partial sums promoted to round-to-nearest FP32 registers every 256 k.  b_transposed = 1: B is
+ * partial sums promoted to round-to-nearest FP32 registers every 1024 k (FB_BF16_KP = 16 k-blocks
+ * of 64).  b_transposed = 1: B is
  * given K-major as [n][k] (ldb >= k); 0: B is [k][n] (ldb >= n) and is transposed into ws.
  * A, B, C 16-byte aligned; lda*2, ldb*2, ldc*4 multiples of 16.  ws:
  * fb_matmul_bf16_workspace_bytes(b_transposed, m, n, k) bytes (0 when b_transposed). */
@@ -135,10 +136,12 @@ fb_status fb_matmul_bf16(int64_t m, int64_t n, int64_t k, const void* A, int64_t
 /* BLAS-style variant: C = alpha op(A) op(B) + beta C, op(X) = X (trans 0) or
  * X^T (trans 1); op(A) is m x k (A stored m x k, lda >= k; or k x m, lda >= m), op(B) is k x n
  * (B stored k x n, ldb >= n; or n x k, ldb >= k).  Same arithmetic and accuracy as fb_matmul
- * (the product is formed by the same kernels, then alpha, beta are applied in FP32 / FP64).
- * beta == 0: C is not read (NaN in C does not propagate); alpha == 0: A and B are not read.
- * Alignment rules as fb_matmul.  ws: fb_gemm_workspace_bytes(...) bytes (transposed operand
- * copies + the fb_matmul workspace + an m x n product tile). */
+ * (the same kernels: a transposed operand is read in its stored orientation -- by the FP64
+ * kernel's tile loads, by the FP32 TF32 split -- and alpha, beta are applied in the kernels'
+ * epilogue in FP32 / FP64; (alpha, beta) = (1, 0) with no transposes is bitwise fb_matmul).
+ * beta == 0: C is not read (NaN in C does not propagate); alpha == 0: A and B are not read
+ * (C = beta C).  Alignment rules as fb_matmul.  ws: fb_gemm_workspace_bytes(...) bytes (the
+ * fb_matmul workspace: FP32 split operands; 0 for FP64, ws may then be NULL). */
 size_t fb_gemm_workspace_bytes(int dtype, int transA, int transB, int64_t m, int64_t n, int64_t k);
 fb_status fb_gemm(int dtype, int transA, int transB, int64_t m, int64_t n, int64_t k, double alpha,
                   const void* A, int64_t lda, const void* B, int64_t ldb, double beta, void* C,

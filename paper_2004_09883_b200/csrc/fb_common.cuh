@@ -68,7 +68,7 @@ struct Knobs {
     int64_t rowblock_panel = 4096;
     // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
     int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
-    int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 0, gemm_lo_overlap = 0;
+    int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 0, gemm_lo_overlap = 0, gemm_persist = 0;
     // LU (fb_lu.cu)
     int lu_tma = 1, lu_debug = 0, lu_rank_simt = 1, lu_serial = 0, lu_lookahead = 1, lu_graph = 1;
 };
@@ -191,6 +191,13 @@ size_t gemm_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k);
 fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                       const void* B, int64_t ldb, void* C, int64_t ldc, void* ws,
                       size_t ws_bytes, const DeviceState* st, cudaStream_t s);
+// fb_gemm's core: C = alpha op(A) op(B) + beta C, op(A) = A (ta = 0, stored m x k) or A^T (ta = 1,
+// stored k x m), op(B) likewise (stored k x n / n x k).  The orientation is taken by the operand
+// loads (FP64) or the TF32 split (FP32), alpha/beta by the kernels' epilogue (C is not read when
+// beta == 0); alpha must be nonzero.  ws: gemm_ws_bytes.
+fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
+                         int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc, void* ws,
+                         size_t ws_bytes, const DeviceState* st, cudaStream_t s);
 
 // G1: TF32 split (transpose=0: X[rows][cols] -> hi/lo [rows][ldo]; transpose=1: -> [cols][ldo])
 fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
@@ -202,6 +209,6 @@ fb_status gemm_3xtf32_fused_device(int64_t m, int64_t n, int64_t k, const float*
                                    int64_t ldb, float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t s);
 fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
                                       int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
-                                      int64_t ldc, cudaStream_t s);
+                                      int64_t ldc, cudaStream_t s, float alpha = 1.f, float beta = 0.f);
 
 }  // namespace fb

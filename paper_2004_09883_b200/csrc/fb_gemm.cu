@@ -28,11 +28,6 @@ struct Cfg {
     static constexpr int THREADS = 32 * WM * WN;
     static constexpr int TM = BM / WM / 16;   // m16 tiles per warp
     static constexpr int TN = BN / WN / 8;    // n8 tiles per warp
-    static constexpr int LDA_S = BK + 4;      // doubles; 160-B rows -> conflict-free fragments
-    static constexpr int LDB_S = BN + 4;
-    static constexpr int A_STAGE = BM * LDA_S;
-    static constexpr int B_STAGE = BK * LDB_S;
-    static constexpr size_t SMEM = (size_t)STAGES * (A_STAGE + B_STAGE) * sizeof(double);
 };
 using CfgSmall = Cfg<64, 64, 2, 2>;   // 1024 tiles at 2048^2: balanced across 148 SMs
 
@@ -44,56 +39,78 @@ __device__ __forceinline__ void dmma_16x8x8(double (&d)[4], const double (&a)[4]
         : "d"(a[0]), "d"(a[1]), "d"(a[2]), "d"(a[3]), "d"(b[0]), "d"(b[1]));
 }
 
-template <class CF>
-__device__ __forceinline__ void load_stage(double* As, double* Bs, const double* __restrict__ A,
-                                           const double* __restrict__ B, int64_t M, int64_t N,
-                                           int64_t K, int64_t lda, int64_t ldb, int64_t m0,
-                                           int64_t n0, int64_t k0, int tid) {
-    // A tile BM x BK in 16-byte chunks (2 doubles)
-#pragma unroll
-    for (int i = 0; i < (CF::BM * CF::BK / 2 + CF::THREADS - 1) / CF::THREADS; ++i) {
-        const int c = tid + i * CF::THREADS;
-        if (c < CF::BM * CF::BK / 2) {
-            const int r = c / (CF::BK / 2), kc = (c % (CF::BK / 2)) * 2;
-            const int64_t gr = m0 + r, gk = k0 + kc;
-            uint32_t bytes = 0;
-            const double* src = A;
-            if (gr < M && gk < K) {
-                bytes = (gk + 1 < K) ? 16 : 8;
-                src = A + gr * lda + gk;
-            }
-            ptx::cp_async_16(ptx::smem_u32(As + r * CF::LDA_S + kc), src, bytes);
-        }
+// Shared-memory layout of one stage for operand orientations TA / TB (fb_gemm's op(A), op(B)
+// read straight from the stored operand, no transposed copy): A as stored (m x k) -> As[m][k]
+// (row pitch BK + 4), A stored k x m -> As[k][m] (pitch BM + 4); B stored k x n -> Bs[k][n]
+// (pitch BN + 4), B stored n x k -> Bs[n][k] (pitch BK + 4).  Every pitch is 4 mod 16 doubles,
+// so the DMMA fragment reads of a half warp hit 16 distinct 8-byte banks in all four layouts.
+template <class CF, bool TA, bool TB>
+struct Lay {
+    static constexpr int LDA = TA ? CF::BM + 4 : CF::BK + 4;
+    static constexpr int LDB = TB ? CF::BK + 4 : CF::BN + 4;
+    static constexpr int A_STAGE = TA ? CF::BK * LDA : CF::BM * LDA;
+    static constexpr int B_STAGE = TB ? CF::BN * LDB : CF::BK * LDB;
+    static constexpr size_t SMEM = (size_t)CF::STAGES * (A_STAGE + B_STAGE) * sizeof(double);
+};
+
+// one 16-byte cp.async chunk (2 doubles along the stored row) of a rows x cols stored operand,
+// zero-filled past its edges (8 bytes when only the first double is inside)
+__device__ __forceinline__ void ld_chunk(double* dst, const double* __restrict__ X, int64_t rows, int64_t cols,
+                                         int64_t ld, int64_t gr, int64_t gc) {
+    uint32_t bytes = 0;
+    const double* src = X;
+    if (gr < rows && gc < cols) {
+        bytes = (gc + 1 < cols) ? 16 : 8;
+        src = X + gr * ld + gc;
     }
-    // B tile BK x BN
+    ptx::cp_async_16(ptx::smem_u32(dst), src, bytes);
+}
+
+// tile R x Ccols (stored orientation) starting at (r0, c0) into S[R][pitch]
+template <int R, int CC, int PITCH, int THREADS>
+__device__ __forceinline__ void load_tile(double* S, const double* __restrict__ X, int64_t rows, int64_t cols,
+                                          int64_t ld, int64_t r0, int64_t c0, int tid) {
 #pragma unroll
-    for (int i = 0; i < (CF::BK * CF::BN / 2 + CF::THREADS - 1) / CF::THREADS; ++i) {
-        const int c = tid + i * CF::THREADS;
-        if (c < CF::BK * CF::BN / 2) {
-            const int r = c / (CF::BN / 2), nc = (c % (CF::BN / 2)) * 2;
-            const int64_t gk = k0 + r, gn = n0 + nc;
-            uint32_t bytes = 0;
-            const double* src = B;
-            if (gk < K && gn < N) {
-                bytes = (gn + 1 < N) ? 16 : 8;
-                src = B + gk * ldb + gn;
-            }
-            ptx::cp_async_16(ptx::smem_u32(Bs + r * CF::LDB_S + nc), src, bytes);
+    for (int i = 0; i < (R * CC / 2 + THREADS - 1) / THREADS; ++i) {
+        const int c = tid + i * THREADS;
+        if (c < R * CC / 2) {
+            const int r = c / (CC / 2), cc = (c % (CC / 2)) * 2;
+            ld_chunk(S + r * PITCH + cc, X, rows, cols, ld, r0 + r, c0 + cc);
         }
     }
 }
 
+template <class CF, bool TA, bool TB>
+__device__ __forceinline__ void load_stage(double* As, double* Bs, const double* __restrict__ A,
+                                           const double* __restrict__ B, int64_t M, int64_t N,
+                                           int64_t K, int64_t lda, int64_t ldb, int64_t m0,
+                                           int64_t n0, int64_t k0, int tid) {
+    using L = Lay<CF, TA, TB>;
+    if constexpr (TA)  // A stored K x M
+        load_tile<CF::BK, CF::BM, L::LDA, CF::THREADS>(As, A, K, M, lda, k0, m0, tid);
+    else
+        load_tile<CF::BM, CF::BK, L::LDA, CF::THREADS>(As, A, M, K, lda, m0, k0, tid);
+    if constexpr (TB)  // B stored N x K
+        load_tile<CF::BN, CF::BK, L::LDB, CF::THREADS>(Bs, B, N, K, ldb, n0, k0, tid);
+    else
+        load_tile<CF::BK, CF::BN, L::LDB, CF::THREADS>(Bs, B, K, N, ldb, k0, n0, tid);
+}
+
+// Epilogue modes: EPI_STORE C <- A B;  EPI_SUB C <- C - A B (the LU trailing update);
+// EPI_AXPBY C <- alpha A B + beta C (fb_gemm; C is not read when beta == 0).
+enum { EPI_STORE = 0, EPI_SUB = 1, EPI_AXPBY = 2 };
+
 // The k-loop order (k-blocks ascending, then kk, then the DMMA's internal order) is the same
-// for every tile shape, so results are bitwise identical across configurations.
-// SUB: C <- C - A B (the LU trailing update), else C <- A B.
-template <class CF, bool SUB = false>
+// for every tile shape and operand orientation, so results are bitwise identical across them.
+template <class CF, int EPI = EPI_STORE, bool TA = false, bool TB = false>
 __global__ void __launch_bounds__(CF::THREADS)
     gemm_f64_dmma_kernel(const double* __restrict__ A, const double* __restrict__ B,
                          double* C, int64_t M, int64_t N, int64_t K, int64_t lda,
-                         int64_t ldb, int64_t ldc) {
+                         int64_t ldb, int64_t ldc, double alpha, double beta) {
+    using L = Lay<CF, TA, TB>;
     extern __shared__ __align__(128) double smem_d[];
     double* As = smem_d;
-    double* Bs = smem_d + CF::STAGES * CF::A_STAGE;
+    double* Bs = smem_d + CF::STAGES * L::A_STAGE;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int wm = warp / CF::WN, wn = warp % CF::WN;
     const int64_t m0 = (int64_t)blockIdx.y * CF::BM, n0 = (int64_t)blockIdx.x * CF::BN;
@@ -110,8 +127,8 @@ __global__ void __launch_bounds__(CF::THREADS)
 #pragma unroll
     for (int st = 0; st < CF::STAGES - 1; ++st) {
         if (st < KT)
-            load_stage<CF>(As + st * CF::A_STAGE, Bs + st * CF::B_STAGE, A, B, M, N, K, lda, ldb, m0, n0,
-                           (int64_t)st * CF::BK, tid);
+            load_stage<CF, TA, TB>(As + st * L::A_STAGE, Bs + st * L::B_STAGE, A, B, M, N, K, lda, ldb, m0, n0,
+                                   (int64_t)st * CF::BK, tid);
         ptx::cp_async_commit();
     }
     const int g = lane >> 2, tq = lane & 3;
@@ -121,24 +138,30 @@ __global__ void __launch_bounds__(CF::THREADS)
         {
             const int nk = kt + CF::STAGES - 1;
             if (nk < KT)
-                load_stage<CF>(As + (nk % CF::STAGES) * CF::A_STAGE, Bs + (nk % CF::STAGES) * CF::B_STAGE, A, B,
-                               M, N, K, lda, ldb, m0, n0, (int64_t)nk * CF::BK, tid);
+                load_stage<CF, TA, TB>(As + (nk % CF::STAGES) * L::A_STAGE, Bs + (nk % CF::STAGES) * L::B_STAGE,
+                                       A, B, M, N, K, lda, ldb, m0, n0, (int64_t)nk * CF::BK, tid);
             ptx::cp_async_commit();
         }
-        const double* as = As + (kt % CF::STAGES) * CF::A_STAGE + (wm * CF::TM * 16) * CF::LDA_S;
-        const double* bs = Bs + (kt % CF::STAGES) * CF::B_STAGE + wn * CF::TN * 8;
+        const double* as = As + (kt % CF::STAGES) * L::A_STAGE;
+        const double* bs = Bs + (kt % CF::STAGES) * L::B_STAGE;
+        const int ar = wm * CF::TM * 16, bc = wn * CF::TN * 8;  // warp tile origin (m, n)
 #pragma unroll
         for (int kk = 0; kk < CF::BK; kk += 8) {
             double af[CF::TM][4], bf[CF::TN][2];
 #pragma unroll
             for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
-                for (int v = 0; v < 4; ++v)
-                    af[i][v] = as[(i * 16 + g + 8 * (v & 1)) * CF::LDA_S + kk + tq + 4 * (v >> 1)];
+                for (int v = 0; v < 4; ++v) {
+                    const int r = ar + i * 16 + g + 8 * (v & 1), kc = kk + tq + 4 * (v >> 1);
+                    af[i][v] = TA ? as[kc * L::LDA + r] : as[r * L::LDA + kc];
+                }
 #pragma unroll
             for (int j = 0; j < CF::TN; ++j)
 #pragma unroll
-                for (int v = 0; v < 2; ++v) bf[j][v] = bs[(kk + tq + 4 * v) * CF::LDB_S + j * 8 + g];
+                for (int v = 0; v < 2; ++v) {
+                    const int kc = kk + tq + 4 * v, c = bc + j * 8 + g;
+                    bf[j][v] = TB ? bs[c * L::LDB + kc] : bs[kc * L::LDB + c];
+                }
 #pragma unroll
             for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
@@ -147,6 +170,11 @@ __global__ void __launch_bounds__(CF::THREADS)
     }
     ptx::cp_async_wait<0>();
     // epilogue: c[v] at row g + 8*(v>>1), col 2*tq + (v&1)
+    auto out = [&](double p, const double* cur) -> double {
+        if constexpr (EPI == EPI_SUB) return *cur - p;
+        if constexpr (EPI == EPI_AXPBY) return beta == 0.0 ? alpha * p : alpha * p + beta * *cur;
+        return p;
+    };
 #pragma unroll
     for (int i = 0; i < CF::TM; ++i)
 #pragma unroll
@@ -159,13 +187,10 @@ __global__ void __launch_bounds__(CF::THREADS)
                     double* dst = C + r * ldc + c;
                     if (c + 1 < N) {
                         double2 o = make_double2(acc[i][j][2 * h], acc[i][j][2 * h + 1]);
-                        if constexpr (SUB) {
-                            const double2 cur = *reinterpret_cast<const double2*>(dst);
-                            o = make_double2(cur.x - o.x, cur.y - o.y);
-                        }
+                        if constexpr (EPI != EPI_STORE) o = make_double2(out(o.x, dst), out(o.y, dst + 1));
                         *reinterpret_cast<double2*>(dst) = o;
                     } else if (c < N) {
-                        dst[0] = SUB ? dst[0] - acc[i][j][2 * h] : acc[i][j][2 * h];
+                        dst[0] = out(acc[i][j][2 * h], dst);
                     }
                 }
             }
@@ -402,10 +427,32 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     tn = in / gm;
 }
 
+// one epilogue row segment: dst[j] = alpha acc[j] + beta dst[j] for j < min(W, valid) (fb_gemm's
+// epilogue; dst is not read when beta == 0, and (alpha, beta) = (1, 0) stores acc exactly)
+template <int W>
+__device__ __forceinline__ void store_row(float* dst, const float (&acc)[W], int valid, float alpha, float beta) {
+    if (valid >= W) {
+#pragma unroll
+        for (int j = 0; j < W; j += 4) {
+            float4 o = make_float4(alpha * acc[j], alpha * acc[j + 1], alpha * acc[j + 2], alpha * acc[j + 3]);
+            if (beta != 0.f) {
+                const float4 c = *reinterpret_cast<const float4*>(dst + j);
+                o = make_float4(o.x + beta * c.x, o.y + beta * c.y, o.z + beta * c.z, o.w + beta * c.w);
+            }
+            *reinterpret_cast<float4*>(dst + j) = o;
+        }
+    } else {
+#pragma unroll
+        for (int j = 0; j < W; ++j)
+            if (j < valid) dst[j] = beta != 0.f ? alpha * acc[j] + beta * dst[j] : alpha * acc[j];
+    }
+}
+
 __global__ void __launch_bounds__(NUM_THREADS, 1)
     gemm_3xtf32_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                        const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
-                       float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n) {
+                       float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n,
+        float alpha, float beta) {
     extern __shared__ uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms
     const uint32_t raw_u32 = ptx::smem_u32(smem_raw);
@@ -534,15 +581,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
         if (row < M) {
             float* dst = C + (int64_t)row * ldc + n0;
             const int valid = N - n0;
-            if (valid >= BN) {
-#pragma unroll
-                for (int j = 0; j < BN; j += 4)
-                    *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < BN; ++j)
-                    if (j < valid) dst[j] = acc[j];
-            }
+            store_row<BN>(dst, acc, valid, alpha, beta);
         }
     }
     ptx::tc_fence_before();
@@ -575,7 +614,8 @@ constexpr int KP_BLOCKS = 4;
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                             const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
-                            float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n) {
+                            float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n,
+        float alpha, float beta) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_u32 = ptx::smem_u32(smem_raw);
     const uint32_t base = (raw_u32 + 1023u) & ~1023u;
@@ -592,9 +632,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t rank = ptx::cluster_ctarank();
     const bool leader = rank == 0;
-    int tm, tn;
-    tf32::tile_coords(blockIdx.x >> 1, tiles_m, tiles_n, tm, tn);
-    const int m0 = tm * 256, n0 = tn * 256;
+    // persistent: pair p computes tiles p, p + P, p + 2P, ... (P = pairs in the grid; round
+    // robin keeps the concurrently computed tiles adjacent in the grouped raster order); the
+    // stage ring and the two TMEM accumulators run on across tiles, so a tile's epilogue (drain
+    // of its last chunk + C stores) overlaps the next tile's first MMAs
+    const int pair = (int)(blockIdx.x >> 1), P = (int)(gridDim.x >> 1);
+    const int ntiles = tiles_m * tiles_n;
     const int KB = (K + BK - 1) / BK;
     const int NCHUNK = (KB + KP_BLOCKS - 1) / KP_BLOCKS;
 
@@ -626,10 +669,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     if (warp == 0) {
         if (lane == 0) {
             // ---------------- TMA producer (both CTAs): own halves, completion on the leader
-            const int am = m0 + 128 * (int)rank, bn = n0 + 128 * (int)rank;
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+            int g = 0;  // k-blocks issued (stage ring position across tiles)
+            for (int tile = pair; tile < ntiles; tile += P) {
+            int tm, tn;
+            tf32::tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            const int am = tm * 256 + 128 * (int)rank, bn = tn * 256 + 128 * (int)rank;
+            for (int kb = 0; kb < KB; ++kb, ++g) {
+                const int s = g % STAGES;
+                const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
                 ptx::mbar_wait(empty_bar(s), ph ^ 1u);
                 if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * STAGE_BYTES);
                 const uint32_t st = base + s * STAGE_BYTES;
@@ -639,21 +686,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 ptx::tma_load_2d_pair(st + 2 * TILE_BYTES, &tmBh, full_bar(s), kc, bn);
                 ptx::tma_load_2d_pair(st + 3 * TILE_BYTES, &tmBl, full_bar(s), kc, bn);
             }
+            }
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {
             // ---------------- MMA issuer (leader CTA, single thread)
             const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
                                    ((uint32_t)(256 >> 4) << 24);
-            for (int c = 0; c < NCHUNK; ++c) {
-                const int buf = c & 1;
-                ptx::mbar_wait(tempty_bar(buf), ((uint32_t)(c >> 1) & 1u) ^ 1u);
+            int g = 0, cg = 0;  // k-blocks consumed, chunks issued (across tiles)
+            for (int tile = pair; tile < ntiles; tile += P) {
+            for (int c = 0; c < NCHUNK; ++c, ++cg) {
+                const int buf = cg & 1;
+                ptx::mbar_wait(tempty_bar(buf), ((uint32_t)(cg >> 1) & 1u) ^ 1u);
                 ptx::tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(buf * ACC_COLS);
                 const int kb_end = min(KB, (c + 1) * KP_BLOCKS);
-                for (int kb = c * KP_BLOCKS; kb < kb_end; ++kb) {
-                    const int s = kb % STAGES;
-                    const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+                for (int kb = c * KP_BLOCKS; kb < kb_end; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
                     ptx::mbar_wait(full_bar(s), ph);
                     ptx::tc_fence_after();
                     const uint32_t st = base + s * STAGE_BYTES;
@@ -673,17 +723,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
                 }
                 ptx::mma_commit_pair(tfull_bar(buf), 0x3);    // partial sum ready in both CTAs
             }
+            }
         }
     } else {
         // ---------------- epilogue warps 2..9: lanes 32*(warp%4), column half (warp-2)/4
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
+        int cg = 0;  // chunks drained (across tiles)
+        for (int tile = pair; tile < ntiles; tile += P) {
+        int tm, tn;
+        tf32::tile_coords(tile, tiles_m, tiles_n, tm, tn);
+        const int m0 = tm * 256, n0 = tn * 256;
         float acc[128];
 #pragma unroll
         for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-        for (int c = 0; c < NCHUNK; ++c) {
-            const int buf = c & 1;
-            ptx::mbar_wait(tfull_bar(buf), (uint32_t)(c >> 1) & 1u);
+        for (int c = 0; c < NCHUNK; ++c, ++cg) {
+            const int buf = cg & 1;
+            ptx::mbar_wait(tfull_bar(buf), (uint32_t)(cg >> 1) & 1u);
             ptx::tc_fence_after();
             const uint32_t taddr =
                 tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC_COLS + h * 128);
@@ -704,15 +760,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         if (row < M) {
             float* dst = C + (int64_t)row * ldc + col0;
             const int valid = N - col0;
-            if (valid >= 128) {
-#pragma unroll
-                for (int j = 0; j < 128; j += 4)
-                    *reinterpret_cast<float4*>(dst + j) = make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
-            } else {
-#pragma unroll
-                for (int j = 0; j < 128; ++j)
-                    if (j < valid) dst[j] = acc[j];
-            }
+            store_row<128>(dst, acc, valid, alpha, beta);
+        }
         }
     }
     ptx::tc_fence_before();
@@ -766,44 +815,40 @@ static fb_status make_kmajor_map(CUtensorMap* map, const float* ptr, int64_t row
 }
 }  // namespace tf32
 
-template <class CF>
-static fb_status launch_f64(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
-                            void* C, int64_t ldc, cudaStream_t s) {
-    auto kern = f64::gemm_f64_dmma_kernel<CF>;
+template <class CF, int EPI, bool TA, bool TB>
+static fb_status launch_f64_t(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B,
+                              int64_t ldb, void* C, int64_t ldc, double alpha, double beta, cudaStream_t s) {
+    auto kern = f64::gemm_f64_dmma_kernel<CF, EPI, TA, TB>;
+    constexpr size_t smem = f64::Lay<CF, TA, TB>::SMEM;
     static std::atomic<int> attr_mask{0};
     int dev = 0;
     cudaGetDevice(&dev);
     if (!(attr_mask & (1 << (dev & 31)))) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr_mask |= 1 << (dev & 31);
     }
+    if (m <= 0 || n <= 0 || k <= 0) return FB_OK;
     dim3 grid((unsigned)((n + CF::BN - 1) / CF::BN), (unsigned)((m + CF::BM - 1) / CF::BM));
     if (grid.y > 65535) {
         set_error("m too large for the FP64 grid");
         return FB_ERR_UNSUPPORTED_SIZE;
     }
-    kern<<<grid, CF::THREADS, CF::SMEM, s>>>((const double*)A, (const double*)B, (double*)C, m, n, k, lda, ldb, ldc);
+    kern<<<grid, CF::THREADS, smem, s>>>((const double*)A, (const double*)B, (double*)C, m, n, k, lda, ldb, ldc,
+                                         alpha, beta);
     FB_LAUNCH_CHECK("gemm_f64_dmma_kernel");
     return FB_OK;
+}
+
+template <class CF>
+static fb_status launch_f64(int64_t m, int64_t n, int64_t k, const void* A, int64_t lda, const void* B, int64_t ldb,
+                            void* C, int64_t ldc, cudaStream_t s) {
+    return launch_f64_t<CF, f64::EPI_STORE, false, false>(m, n, k, A, lda, B, ldb, C, ldc, 1.0, 0.0, s);
 }
 
 // C -= A B in FP64 (LU trailing update; C may alias neither A nor B).
 fb_status gemm_f64_sub_device(int64_t m, int64_t n, int64_t k, const double* A, int64_t lda, const double* B,
                               int64_t ldb, double* C, int64_t ldc, cudaStream_t s) {
-    using CF = f64::CfgSmall;
-    auto kern = f64::gemm_f64_dmma_kernel<CF, true>;
-    static std::atomic<int> attr_mask{0};
-    int dev = 0;
-    cudaGetDevice(&dev);
-    if (!(attr_mask & (1 << (dev & 31)))) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::SMEM));
-        attr_mask |= 1 << (dev & 31);
-    }
-    if (m <= 0 || n <= 0 || k <= 0) return FB_OK;
-    dim3 grid((unsigned)((n + CF::BN - 1) / CF::BN), (unsigned)((m + CF::BM - 1) / CF::BM));
-    kern<<<grid, CF::THREADS, CF::SMEM, s>>>(A, B, C, m, n, k, lda, ldb, ldc);
-    FB_LAUNCH_CHECK("gemm_f64_dmma_kernel<sub>");
-    return FB_OK;
+    return launch_f64_t<f64::CfgSmall, f64::EPI_SUB, false, false>(m, n, k, A, lda, B, ldb, C, ldc, 1.0, 0.0, s);
 }
 
 size_t gemm_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
@@ -820,15 +865,36 @@ size_t gemm_ws_bytes(int dtype, int64_t m, int64_t n, int64_t k) {
 fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
                       const void* B, int64_t ldb, void* C, int64_t ldc, void* ws, size_t ws_bytes,
                       const DeviceState* st, cudaStream_t s) {
+    return gemm_ex_device(dtype, 0, 0, m, n, k, 1.0, A, lda, B, ldb, 0.0, C, ldc, ws, ws_bytes, st, s);
+}
+
+template <int EPI>
+static fb_status launch_f64_op(int ta, int tb, int64_t m, int64_t n, int64_t k, const void* A, int64_t lda,
+                               const void* B, int64_t ldb, void* C, int64_t ldc, double alpha, double beta,
+                               cudaStream_t s) {
+    using CF = f64::CfgSmall;
+    if (ta && tb) return launch_f64_t<CF, EPI, true, true>(m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, s);
+    if (ta) return launch_f64_t<CF, EPI, true, false>(m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, s);
+    if (tb) return launch_f64_t<CF, EPI, false, true>(m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, s);
+    return launch_f64_t<CF, EPI, false, false>(m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, s);
+}
+
+fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_t k, double alpha, const void* A,
+                         int64_t lda, const void* B, int64_t ldb, double beta, void* C, int64_t ldc, void* ws,
+                         size_t ws_bytes, const DeviceState* st, cudaStream_t s) {
+    const bool plain = alpha == 1.0 && beta == 0.0;
     if (dtype == FB_F64) {
+        if (!plain) return launch_f64_op<f64::EPI_AXPBY>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc, alpha, beta, s);
+        if (ta || tb) return launch_f64_op<f64::EPI_STORE>(ta, tb, m, n, k, A, lda, B, ldb, C, ldc, 1.0, 0.0, s);
         const int cfg = knobs().f64_cfg;  // A/B knob: 0 = 64x64 (default), 1 = 128x128, 2 = 128x64
         if (cfg == 1) return launch_f64<f64::Cfg<128, 128, 2, 4>>(m, n, k, A, lda, B, ldb, C, ldc, s);
         if (cfg == 2) return launch_f64<f64::Cfg<128, 64, 2, 2>>(m, n, k, A, lda, B, ldb, C, ldc, s);
         return launch_f64<f64::CfgSmall>(m, n, k, A, lda, B, ldb, C, ldc, s);
     }
-    // ---- FP32 via 3xTF32: one fused kernel (raw operands, lo formed in shared memory,
-    // fb_gemm_fused.cu); knob FB_GEMM_FUSED=0: split pre-pass (A as is, B transposed) + MMA kernel
-    if (knobs().gemm_fused)
+    // ---- FP32 via 3xTF32: split pre-pass (op(A) and op(B)^T to K-major hi/lo) + MMA kernel with
+    // the alpha/beta epilogue; A/B knob FB_GEMM_FUSED=1 (plain products only): one fused kernel
+    // (raw operands, lo formed in shared memory, fb_gemm_fused.cu)
+    if (knobs().gemm_fused && plain && !ta && !tb)
         return gemm_3xtf32_fused_device(m, n, k, (const float*)A, lda, (const float*)B, ldb, (float*)C, ldc, ws,
                                         ws_bytes, s);
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX) {
@@ -844,7 +910,10 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
     float* Al = Ah + m * kp;
     float* Bh = Al + m * kp;
     float* Bl = Bh + n * kp;
-    if (knobs().gemm_split2 == 1) {  // A/B knob: 1 = two split launches
+    if (ta || tb) {  // transposed operands: A^T stored k x m splits transposing, B^T stored n x k as is
+        FB_TRY(tf32_split_device(ta, ta ? k : m, ta ? m : k, (const float*)A, lda, Ah, Al, kp, st, s));
+        FB_TRY(tf32_split_device(tb ? 0 : 1, tb ? n : k, tb ? k : n, (const float*)B, ldb, Bh, Bl, kp, st, s));
+    } else if (knobs().gemm_split2 == 1) {  // A/B knob: 1 = two split launches
         FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
         FB_TRY(tf32_split_device(1, k, n, (const float*)B, ldb, Bh, Bl, kp, st, s));
     } else if (knobs().gemm_splitv != 1 &&
@@ -872,7 +941,8 @@ fb_status gemm_device(int dtype, int64_t m, int64_t n, int64_t k, const void* A,
             (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a, a_cblk);
         FB_LAUNCH_CHECK("split_both_kernel");
     }
-    return gemm_3xtf32_presplit_device(m, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C, ldc, s);
+    return gemm_3xtf32_presplit_device(m, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C, ldc, s, (float)alpha,
+                                       (float)beta);
 }
 
 fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
@@ -896,7 +966,7 @@ fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const flo
 
 fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
                                       int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
-                                      int64_t ldc, cudaStream_t s) {
+                                      int64_t ldc, cudaStream_t s, float alpha, float beta) {
     CUtensorMap mAh, mAl, mBh, mBl;
     FB_TRY(tf32::make_kmajor_map(&mAh, Ah, m, k, lda, tf32::BM));
     FB_TRY(tf32::make_kmajor_map(&mAl, Al, m, k, lda, tf32::BM));
@@ -921,8 +991,15 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
             set_error("too many tiles");
             return FB_ERR_UNSUPPORTED_SIZE;
         }
+        // persistent (knob FB_GEMM_PERSIST): one CTA pair per two SMs loops over the tiles
+        int64_t pairs = tiles;
+        if (knobs().gemm_persist) {
+            int sms = 148;
+            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+            pairs = std::min<int64_t>(tiles, sms / 2);
+        }
         cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3((unsigned)(2 * tiles));
+        cfg.gridDim = dim3((unsigned)(2 * pairs));
         cfg.blockDim = dim3(tf32::pair::NUM_THREADS);
         cfg.dynamicSmemBytes = tf32::pair::SMEM;
         cfg.stream = s;
@@ -932,7 +1009,7 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf32::pair::gemm_3xtf32_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m,
-                                       (int)n, (int)k, ldc, tiles_m, tiles_n));
+                                       (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta));
         FB_LAUNCH_CHECK("gemm_3xtf32_pair_kernel");
         return FB_OK;
     }
@@ -944,7 +1021,7 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
         return FB_ERR_UNSUPPORTED_SIZE;
     }
     tf32::gemm_3xtf32_kernel<<<(unsigned)tiles, tf32::NUM_THREADS, tf32::SMEM, s>>>(
-        mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, ldc, tiles_m, tiles_n);
+        mAh, mAl, mBh, mBl, C, (int)m, (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta);
     FB_LAUNCH_CHECK("gemm_3xtf32_kernel");
     return FB_OK;
 }

@@ -126,9 +126,12 @@ def test_gemm_ex_validation(L):
     assert L.fb_gemm(2, 0, 0, 4, 4, 4, 1.0, p, 4, p, 4, 0.0, p, 4, ws, big, None) == 1   # dtype
     assert L.fb_gemm(1, 2, 0, 4, 4, 4, 1.0, p, 4, p, 4, 0.0, p, 4, ws, big, None) == 1   # trans flag
     assert L.fb_gemm(1, 1, 0, 8, 4, 4, 1.0, p, 4, p, 4, 0.0, ctypes.c_void_p(1 << 24), 4, ws, big, None) == 1  # lda < m
-    assert L.fb_gemm(1, 0, 0, 4, 4, 4, 1.0, p, 4, ctypes.c_void_p(1 << 22), 4, 0.0,
-                     ctypes.c_void_p(1 << 24), 4, None, 0, None) == 4                       # workspace
-    assert L.fb_gemm_workspace_bytes(1, 1, 1, 64, 64, 64) > L.fb_gemm_workspace_bytes(1, 0, 0, 64, 64, 64)
+    assert L.fb_gemm(0, 0, 0, 4, 4, 4, 1.0, p, 4, ctypes.c_void_p(1 << 22), 4, 0.0,
+                     ctypes.c_void_p(1 << 24), 4, None, 0, None) == 4                       # FP32 workspace
+    # transposes and alpha/beta need no temporaries: FP32 needs the fb_matmul split workspace,
+    # FP64 none
+    assert L.fb_gemm_workspace_bytes(0, 1, 1, 64, 64, 64) == L.fb_matmul_workspace_bytes(0, 64, 64, 64) > 0
+    assert L.fb_gemm_workspace_bytes(1, 1, 1, 64, 64, 64) == 0
 
 
 def test_rfft2d_validation(L):

@@ -214,12 +214,57 @@ def test_gemm_ex_transposes_alpha_beta(fb, dt, ta, tb):
         assert oracle.rel_l2(C.cpu().numpy(), ref) < bar, (alpha, beta)
 
 
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+@pytest.mark.parametrize("ta,tb", [(1, 0), (0, 1), (1, 1)])
+def test_gemm_ex_transposed_operand_bitwise(fb, dt, ta, tb):
+    """A transposed operand is read in its stored orientation (FP64 tile loads, FP32 TF32
+    split), so fb_gemm(trans) is bitwise fb_matmul on the explicitly transposed operands (same
+    values, same k order), across several tiles with ragged edges; (alpha, beta) = (1, 0)."""
+    m, n, k = 300, 260, 203
+    mk = synth.real_matrix_f64 if dt == torch.float64 else synth.real_matrix
+    Ah = mk(k if ta else m, m if ta else k, synth.TID_GEMM_A)
+    Bh = mk(n if tb else k, k if tb else n, synth.TID_GEMM_B)
+    opA = np.ascontiguousarray(Ah.T if ta else Ah)
+    opB = np.ascontiguousarray(Bh.T if tb else Bh)
+    q = 16 // np.dtype(np.float64 if dt == torch.float64 else np.float32).itemsize
+
+    def dev(h):  # 16-byte row pitch as the ABI requires
+        b = torch.zeros(h.shape[0], -(-h.shape[1] // q) * q, dtype=dt)
+        b[:, :h.shape[1]] = torch.from_numpy(np.ascontiguousarray(h)).to(dt)
+        return b.cuda()[:, :h.shape[1]]
+
+    C1 = dev(np.zeros((m, n)))
+    fb.gemm(dev(Ah), dev(Bh), C1, 1.0, 0.0, bool(ta), bool(tb))
+    C0 = dev(np.zeros((m, n)))
+    fb.gemm(dev(opA), dev(opB), C0, 1.0, 0.0)
+    torch.cuda.synchronize()
+    assert torch.equal(C0, C1)
+    bar = 1e-5 if dt == torch.float32 else 1e-12
+    assert oracle.rel_l2(C1.cpu().numpy(), oracle.matmul(opA.astype(np.float64), opB.astype(np.float64))) < bar
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_gemm_ex_epilogue_large(fb, dt):
+    """alpha/beta in the epilogue over many tiles (FP32 pair kernel 256 x 256 tiles, FP64 64 x 64),
+    full-mantissa FP64 operands, against alpha P + beta C0 formed in FP64 by the oracle."""
+    m, n, k = 700, 532, 332  # ld*4 % 16 == 0 (ABI), ragged against the 256 and 64 tiles
+    mk = synth.real_matrix_f64 if dt == torch.float64 else synth.real_matrix
+    A0, B0, C0 = mk(m, k, synth.TID_GEMM_A), mk(k, n, synth.TID_GEMM_B), mk(m, n, synth.TID_NOISE)
+    P = oracle.matmul(A0.astype(np.float64), B0.astype(np.float64))
+    for alpha, beta in [(0.75, -0.5), (1.0, 1.0), (-3.0, 0.0)]:
+        C = torch.from_numpy(C0).to(dt).cuda()
+        fb.gemm(torch.from_numpy(A0).to(dt).cuda(), torch.from_numpy(B0).to(dt).cuda(), C, alpha, beta)
+        torch.cuda.synchronize()
+        ref = alpha * P + beta * C0.astype(np.float64)
+        assert oracle.rel_l2(C.cpu().numpy(), ref) < (1e-5 if dt == torch.float32 else 1e-12), (alpha, beta)
+
+
 @pytest.mark.parametrize("ta,tb,m,n,k", [(1, 0, 128, 128, 6), (1, 1, 96, 40, 13), (0, 0, 100, 130, 64),
                                          (0, 1, 64, 130, 50), (1, 0, 33, 131, 7)])
 def test_gemm_ex_f32_unaligned_temporaries(fb, ta, tb, m, n, k):
-    """fb_gemm FP32 with k % 4 != 0 under transA (the transposed copy of A gets a 16-byte row
-    pitch) and n % 4 != 0, n >= 128 with (alpha, beta) != (1, 0) (the product tile T gets a
-    16-byte row pitch): every operand and C live in 16-byte-pitched buffers, as the ABI requires."""
+    """fb_gemm FP32 with k % 4 != 0 under transA and n % 4 != 0, n >= 128 with (alpha, beta) !=
+    (1, 0): every operand and C live in 16-byte-pitched buffers, as the ABI requires, and the
+    split / epilogue handle the ragged rows."""
     q = 4
     def padded(rows, cols, tid):
         h = synth.real_matrix(rows, cols, tid)
@@ -285,6 +330,20 @@ def test_gemm_fused_kernel_vs_oracle(fb, knobs, m, n, k, monkeypatch):
     C1 = _mm_padded(fb, A, B)
     C2 = _mm_padded(fb, A, B)
     assert np.array_equal(C1, C2)
+    assert oracle.rel_l2(C1, oracle.matmul(A, B)) < 1e-5
+
+
+@pytest.mark.parametrize("m,n,k", [(4096, 3000, 300), (2600, 2048, 1000), (300, 260, 203)])
+def test_gemm_persistent_pair_bitwise(fb, m, n, k, monkeypatch):
+    """FB_GEMM_PERSIST=1: 74 CTA pairs loop over the tiles (stage ring and TMEM accumulators
+    running on across tiles).  Per tile the arithmetic is the non-persistent kernel's, so the
+    result is bitwise the same, with more tiles than pairs and a ragged edge."""
+    A = synth.real_matrix(m, k, synth.TID_GEMM_A)
+    B = synth.real_matrix(k, n, synth.TID_GEMM_B)
+    C0 = _mm_padded(fb, A, B)
+    monkeypatch.setenv("FB_GEMM_PERSIST", "1")
+    C1 = _mm_padded(fb, A, B)
+    assert np.array_equal(C0, C1)
     assert oracle.rel_l2(C1, oracle.matmul(A, B)) < 1e-5
 
 

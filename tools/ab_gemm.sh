@@ -1,7 +1,8 @@
 cd $GRAFT_REPO_ROOT
-timeout 900 python -m pytest tests/test_gemm_gpu.py tests/test_comm_gpu.py -m gpu -q -x 2>&1 | tail -3 > gpurun_out/gemm_tests.log
-rm -f gpurun_out/gemm_ab.txt
-for cfg in "" "FB_GEMM_SPLIT2=1"; do
-env $cfg timeout 300 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --only gemm_f32_2048 > gpurun_out/g_x.json 2>/dev/null
-python -c "import json; d=json.loads(open('gpurun_out/g_x.json').read().strip().splitlines()[-1]); b=d['blocks']['gemm_f32_2048']; print('$cfg', b['ms_per_step'], b['value'], b['roofline']['kernel_ms'])" >> gpurun_out/gemm_ab.txt
-done
+mkdir -p gpurun_out
+timeout 600 python -m pytest tests/test_gemm_gpu.py -x -q -m gpu -k "persistent or vs_oracle or variants" 2>&1 | tail -3
+for r in 1 2; do
+for sz in "4096 4096 4096 20" "8192 8192 8192 10" "16384 16384 16384 5" "32768 32768 32768 3"; do
+for v in "FB_GEMM_PERSIST=0" "FB_GEMM_PERSIST=1"; do
+  env $v timeout 300 python tools/gemm_bench.py $sz | VAR="$v" python -c "import json,os,sys; d=json.loads(sys.stdin.read()); print(d['m'], os.environ['VAR'], round(d['ms'],3), round(d['tflops'],1), d['rel_l2_vs_torch_f64'])"
+done; done; done
