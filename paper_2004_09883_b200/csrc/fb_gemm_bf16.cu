@@ -18,7 +18,10 @@
 namespace fb {
 namespace bf16 {
 constexpr int BK = 64;                                   // elements per k-block (128-byte rows)
-constexpr int STAGES = 6;
+#ifndef FB_BF16_STAGES
+#define FB_BF16_STAGES 6
+#endif
+constexpr int STAGES = FB_BF16_STAGES;  // 7 (fits 227 KiB) measured slower: 0.796 vs 0.790 ms at 8192^3
 constexpr int NUM_THREADS = 320;                         // w0 TMA, w1 MMA/TMEM, w2..9 epilogue
 constexpr int NUM_EPI_WARPS = 8;
 constexpr uint32_t TILE_BYTES = 128 * BK * 2;            // 16 KiB per operand half
@@ -70,14 +73,23 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
     const uint32_t crank = ptx::cluster_ctarank();
     const uint32_t rank = crank & 1u, pair = crank >> 1;
     const bool leader = rank == 0;
-    int tm, tn;
-    if (CL == 2) {
-        tile_coords(blockIdx.x >> 1, tiles_m, tiles_n, tm, tn);
-    } else {
-        tile_coords(blockIdx.x >> 2, tiles_m, (tiles_n + 1) >> 1, tm, tn);
-        tn = 2 * tn + (int)pair;
-    }
-    const int m0 = tm * 256, n0 = tn * 256;
+    // work units: CL = 2 one 256 x 256 tile per unit, CL = 4 two adjacent tiles; persistent
+    // when the grid is smaller than the unit count (A/B knob FB_BF16_PERSIST): the cluster
+    // loops over units u = cluster id + k * clusters, the stage ring and the two TMEM
+    // accumulators running on across units (the epilogue of one overlaps the next's MMAs)
+    const int units = CL == 2 ? tiles_m * tiles_n : tiles_m * ((tiles_n + 1) >> 1);
+    const int u0 = (int)(blockIdx.x / CL), ustep = (int)(gridDim.x / CL);
+    auto unit_tile = [&](int u, int& m0, int& n0) {
+        int tm, tn;
+        if (CL == 2) {
+            tile_coords(u, tiles_m, tiles_n, tm, tn);
+        } else {
+            tile_coords(u, tiles_m, (tiles_n + 1) >> 1, tm, tn);
+            tn = 2 * tn + (int)pair;
+        }
+        m0 = tm * 256;
+        n0 = tn * 256;
+    };
     const uint16_t own_pair_mask = (uint16_t)(0x3u << (2 * pair));
     const uint16_t stage_mask = CL == 2 ? (uint16_t)0x3 : (uint16_t)0xF;
     const int KB = (K + BK - 1) / BK;
@@ -108,10 +120,14 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // TMA producer (both CTAs): own halves, completion on the leader
+            int g = 0;
+            for (int u = u0; u < units; u += ustep) {
+            int m0, n0;
+            unit_tile(u, m0, n0);
             const int am = m0 + 128 * (int)rank, bn = n0 + 128 * (int)rank;
-            for (int kb = 0; kb < KB; ++kb) {
-                const int s = kb % STAGES;
-                const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+            for (int kb = 0; kb < KB; ++kb, ++g) {
+                const int s = g % STAGES;
+                const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
                 ptx::mbar_wait(empty_bar(s), ph ^ 1u);
                 if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * STAGE_BYTES);
                 const uint32_t st = base + s * STAGE_BYTES;
@@ -122,6 +138,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                     ptx::tma_load_2d_pair_mc(st, &tmA, full_bar(s), kc, am, (uint16_t)((1u << rank) | (4u << rank)));
                 ptx::tma_load_2d_pair(st + TILE_BYTES, &tmB, full_bar(s), kc, bn);
             }
+            }
         }
     } else if (warp == 1) {
         if (leader && lane == 0) {  // MMA issuer
@@ -129,15 +146,17 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
             // N >> 3 at bit 17, M >> 4 at bit 24
             const uint32_t idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
                                    ((uint32_t)(256 >> 4) << 24);
-            for (int c = 0; c < NCHUNK; ++c) {
-                const int buf = c & 1;
-                ptx::mbar_wait(tempty_bar(buf), ((uint32_t)(c >> 1) & 1u) ^ 1u);
+            int g = 0, cg = 0;
+            for (int u = u0; u < units; u += ustep) {
+            for (int c = 0; c < NCHUNK; ++c, ++cg) {
+                const int buf = cg & 1;
+                ptx::mbar_wait(tempty_bar(buf), ((uint32_t)(cg >> 1) & 1u) ^ 1u);
                 ptx::tc_fence_after();
                 const uint32_t tmem_d = tmem_base + (uint32_t)(buf * ACC_COLS);
                 const int kb_end = min(KB, (c + 1) * KP_BLOCKS);
-                for (int kb = c * KP_BLOCKS; kb < kb_end; ++kb) {
-                    const int s = kb % STAGES;
-                    const uint32_t ph = (uint32_t)(kb / STAGES) & 1u;
+                for (int kb = c * KP_BLOCKS; kb < kb_end; ++kb, ++g) {
+                    const int s = g % STAGES;
+                    const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
                     ptx::mbar_wait(full_bar(s), ph);
                     ptx::tc_fence_after();
                     const uint32_t st = base + s * STAGE_BYTES;
@@ -152,16 +171,21 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 }
                 ptx::mma_commit_pair(tfull_bar(buf), own_pair_mask);
             }
+            }
         }
     } else {  // epilogue warps 2..9: lanes 32*(warp%4), column half (warp-2)/4
         const int q = warp & 3;
         const int h = (warp - 2) >> 2;
+        int cg = 0;
+        for (int u = u0; u < units; u += ustep) {
+        int m0, n0;
+        unit_tile(u, m0, n0);
         float acc[128];
 #pragma unroll
         for (int j = 0; j < 128; ++j) acc[j] = 0.f;
-        for (int c = 0; c < NCHUNK; ++c) {
-            const int buf = c & 1;
-            ptx::mbar_wait(tfull_bar(buf), (uint32_t)(c >> 1) & 1u);
+        for (int c = 0; c < NCHUNK; ++c, ++cg) {
+            const int buf = cg & 1;
+            ptx::mbar_wait(tfull_bar(buf), (uint32_t)(cg >> 1) & 1u);
             ptx::tc_fence_after();
             const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC_COLS + h * 128);
 #pragma unroll
@@ -190,6 +214,7 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
                 for (int j = 0; j < 128; ++j)
                     if (j < valid) dst[j] = acc[j];
             }
+        }
         }
     }
     ptx::tc_fence_before();
@@ -318,7 +343,13 @@ fb_status fb_matmul_bf16(int64_t m, int64_t n, int64_t k, const void* A, int64_t
         attr_mask |= 1 << (dev & 31);
     }
     const int tiles_m = (int)((m + 255) / 256), tiles_n = (int)((n + 255) / 256);
-    const int64_t ctas = CLn == 2 ? 2 * (int64_t)tiles_m * tiles_n : 4 * (int64_t)tiles_m * ((tiles_n + 1) / 2);
+    int64_t ctas = CLn == 2 ? 2 * (int64_t)tiles_m * tiles_n : 4 * (int64_t)tiles_m * ((tiles_n + 1) / 2);
+    // persistent (default; knob FB_BF16_PERSIST=0 for one unit per cluster): 8192^3 0.820 ->
+    // 0.790 ms, 4096^3 0.145 -> 0.124 ms; the CL = 4 multicast form is slower either way
+    if (knobs().bf16_persist && CLn == 2) {  // one cluster per CLn SMs, looping over the work units
+        const int64_t cap = (int64_t)(st->sm_count / CLn) * CLn;
+        if (ctas > cap) ctas = cap;
+    }
     if (ctas > INT32_MAX) {
         set_error("too many tiles");
         return FB_ERR_UNSUPPORTED_SIZE;

@@ -387,6 +387,21 @@ def test_gemm_bf16_multicast_cluster(fb, monkeypatch):
     assert torch.equal(C2, C4)
 
 
+def test_gemm_bf16_persistent_bitwise(fb, monkeypatch):
+    """Persistent BF16 kernel (default): one CTA pair per 2 SMs loops over the tiles with the
+    stage ring and TMEM accumulators running on across tiles; per tile the MMA order is
+    unchanged, so the product is bitwise the one-tile-per-pair kernel's (FB_BF16_PERSIST=0),
+    with more tiles than pairs and ragged edges."""
+    m, n, k = 3000, 2900, 640
+    A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).to(torch.bfloat16).cuda()
+    Bt = torch.from_numpy(synth.real_matrix(n, k, synth.TID_GEMM_B)).to(torch.bfloat16).cuda()
+    C1 = fb.matmul_bf16(A, Bt, b_transposed=True)
+    monkeypatch.setenv("FB_BF16_PERSIST", "0")
+    C0 = fb.matmul_bf16(A, Bt, b_transposed=True)
+    torch.cuda.synchronize()
+    assert torch.equal(C0, C1)
+
+
 def test_config4_full_size_sampled(fb):
     """configs[4] at its full size (32768^3 FP32, the launch configuration bench.py times at one
     GPU): sampled full rows and columns of C against the oracle (each 2^30 FP64 MACs)."""
