@@ -66,7 +66,7 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
 // CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B): atoms of 32 MN elements (128 B) x 4 k rows, so
 // LBO = distance between 32-element MN chunks (4 KiB here: each chunk is a [32 k][32 n] TMA
 // box) and SBO = distance between 4-row k groups (512 B).  Verified on the GPU against the
-// other candidate encodings (tools/dbg_gemm.py: only this one reproduces A B).
+// other candidate encodings (tools/experiments/dbg_gemm.py: only this one reproduces A B).
 __device__ __forceinline__ uint64_t smem_desc_mnmajor_sw128b32(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
