@@ -68,14 +68,15 @@ def cpu_model() -> str:
     return "unknown"
 
 
-def ncu_traffic(kernel: str, workload: str):
-    """dram bytes per launch from a committed `ncu --set full` summary, if present."""
+def ncu_traffic(workload: str):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the workload's dominant kernel(s),
+    from the committed `ncu --set full` summaries (profiles/ncu_traffic.json, written by
+    tools/ncu_summarize.py), if present."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
-    d = json.load(open(p))
-    v = d.get(workload, {}).get(kernel)
-    return None if v is None else float(v)
+    vals = list(json.load(open(p)).get(workload, {}).values())
+    return float(vals[0]) if vals else None
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -289,7 +290,7 @@ def main():
                                  "kernel": "fft_pass_tma_kernel (row pass) + fft_col1024_kernel (column pass)",
                                  "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                  "frac": achieved / pk["hbm_gbs"],
-                                 "traffic": ncu_traffic("fft_pass_kernel", "fft2d_2048"),
+                                 "traffic": ncu_traffic("fft2d_2048"),
                                  "algorithmic_bytes_per_launch": bytes_launch,
                                  "launches_per_step": launches, "peak_source": pk["source"]},
                     "gpu_launches": launches * args.steps, "clocks": clk.summary()})
@@ -401,7 +402,7 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                          "achieved": 3 * flops / (tk * 1e-3) / 1e12, "peak": tf32_peak, "unit": "TFLOP/s",
                          "frac": 3 * flops / (tk * 1e-3) / 1e12 / tf32_peak,
                          "note": "achieved counts the 3 TF32 MMAs (6MNK); useful 2MNK = achieved/3",
-                         "traffic": ncu_traffic("gemm_3xtf32_kernel", "gemm_2048"),
+                         "traffic": ncu_traffic("gemm_2048"),
                          "whole_call_frac": 3 * flops / (t * 1e-3) / 1e12 / tf32_peak,
                          "peak_source": tcp["source"] + " -- TF32 burst, data operands"}}
         del A, B, C, ws, Ah, Al, Bh, Bl
@@ -418,6 +419,7 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
             "config": {"workload": "gemm_2048^3_fp64_dmma", "configs_index": 2},
             "roofline": {"bound": "tensor", "kernel": "gemm_f64_dmma_kernel", "achieved": flops / (t * 1e-3) / 1e12,
                          "peak": f64_peak, "unit": "TFLOP/s", "frac": flops / (t * 1e-3) / 1e12 / f64_peak,
+                         "traffic": ncu_traffic("gemm_f64_2048"),
                          "peak_source": tc_peaks()["source"] + " -- FP64 DMMA"}}
         del A, B, C
     # the paper's own matrix workload, LU of a 2048x2048 orthogonal matrix
@@ -474,6 +476,7 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                               "config": {"workload": "fft2d_16384x16384_fwd_1gpu", "configs_index": 3},
                               "roofline": {"bound": "hbm", "achieved": ach, "peak": pk["hbm_gbs"], "unit": "GB/s",
                                            "frac": ach / pk["hbm_gbs"],
+                                           "traffic_row_pass": ncu_traffic("fft2d_16384"),
                                            "note": "algorithmic 2 passes x (R+W) of the 2 GiB array = 8 GiB "
                                                    "(SURVEY 8(d)); the implementation moves 3 passes (four-step "
                                                    "16384-long columns)"}}
@@ -493,6 +496,7 @@ def extra_blocks(args, torch, fb, synth, np, stream, flush, pk, only):
                                             "b_layout": "K-major (B^T given)"},
                                  "roofline": {"bound": "tensor", "achieved": tf, "peak": pk["bf16_tflops"],
                                               "unit": "TFLOP/s", "frac": tf / pk["bf16_tflops"],
+                                              "traffic": ncu_traffic("gemm_bf16_8192"),
                                               "peak_source": pk["source"] + " (BF16 burst)"}}
         del A, Bt, C
     if want("gemm_f32_32768"):  # configs[4] at 1 GPU: the scaling baseline of the row-block GEMM

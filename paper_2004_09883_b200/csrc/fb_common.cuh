@@ -62,7 +62,7 @@ struct Knobs {
     int fft_4step_lb = -1, fft_pair = 1, fft_pair_max_log2 = 11, fft_no_tma_col = 0, fft_col_c = 0;
     int fft_no_tma_row = 0, fft_col_nb = 0, fft_row_nb = 0, fft_no_tma = 0, fft_longrow = 1, fft_pair_tma = 1;
     int fft_no_pdl = 0, fft_debug = 0, fft_sub = 0;  // FB_FFT_SUB: 0 auto, 1 / 3 forced
-    int fft_sub_ilv = 0, fft_col32 = 1, fft_row16k = 1;
+    int fft_sub_ilv = 0, fft_col32 = 1, fft_row16k = 1, fft_row16k_cps = 2;
     // multi-GPU (fb_comm.cu)
     int slab_fused = 1;
     int64_t rowblock_panel = 4096;

@@ -1466,6 +1466,143 @@ static fb_status launch_row16384(const FftPass& p, const DeviceState* st, cudaSt
                       (const float2*)st->twiddles);
 }
 
+// -------------------------------------------------------------------------------------
+// The same 32 x 32 x 16 four-step with each line split over a CTA PAIR (cluster of 2,
+// 256 threads each), so that two or three half-line CTAs of different lines share an SM and
+// their load / exchange / store phases interleave (one 512-thread CTA per SM holding a whole
+// 128 KiB line cannot overlap them).  CTA r:
+//   A  thread j: t = 256 r + j, the length-32 DFT over m of x[t + 512 m], times
+//      W_16384^{t k1}; y[t][k1] goes to the CTA owning k1 (k1 >> 4): E1[k1 & 15][t] (pitch
+//      513), half of it through distributed shared memory;
+//   B  thread (k1l = j & 15, t1 = j >> 4), k1 = 16 r + k1l: the length-32 DFT over t2 of
+//      E1[k1l][t1 + 16 t2], times W_512^{t1 k2b} -> E2[k2b][t1][k1l] (aliases E1);
+//   C  thread (k1l, k2b in {2 (j >> 4), 2 (j >> 4) + 1}): the length-16 DFT over t1 ->
+//      X[k1 + 32 k2b + 1024 c].
+// Per element the operations are those of fft_row16384_kernel, so the results are bitwise
+// equal.  Two cluster barriers per line: after the remote writes (release / acquire), and a
+// split one whose arrive follows stage C's reads of E2 and whose wait precedes the next line's
+// remote writes, so the peer's reads of the previous line overlap this CTA's loads and stage A.
+constexpr int kL14cThreads = 256;
+constexpr int kL14cP1 = 513;
+constexpr size_t kL14cSmem = (size_t)16 * kL14cP1 * sizeof(float2) + 16;
+
+template <bool OUT_GENERIC, int CPS>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kL14cThreads, CPS)
+    fft_row16384c_kernel(const FftPass p, const float2* __restrict__ tw) {
+    extern __shared__ __align__(128) float2 smf[];
+    float2* E = smf;
+    const int j = threadIdx.x;
+    const uint32_t r = ptx::cluster_ctarank();
+    const uint32_t e_loc = ptx::smem_u32(E);
+    const uint32_t e_peer = ptx::mapa_shared(e_loc, r ^ 1u);
+    ptx::pdl_launch_dependents();
+    ptx::pdl_wait();
+    const int64_t nl = p.nlines;
+    const int64_t ncl = gridDim.x >> 1;
+    const int t = 256 * (int)r + j;
+    ptx::cluster_arrive_release();  // "E free" for the first line
+    for (int64_t g = blockIdx.x >> 1; g < nl; g += ncl) {
+        const int64_t gn = g + ncl;
+        if (j == 0 && gn < nl)  // this CTA's half of the next line into L2
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p.in + gn * p.lin.hi + 8192 * r),
+                         "r"(8192u * 8u)
+                         : "memory");
+        float2 v[32];
+        {
+            const float2* src = p.in + g * p.lin.hi + t;
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m] = __ldcs(src + 512 * m);
+        }
+        if (p.conj_in) {
+#pragma unroll
+            for (int m = 0; m < 32; ++m) v[m].y = -v[m].y;
+        }
+        // ---- A
+        dft<32>(v);
+        {
+            float2 bA[5];
+#pragma unroll
+            for (int i = 0; i < 5; ++i) bA[i] = __ldg(tw + ((t << i) & (kTwN - 1)));
+            apply_pow32(v, bA);
+        }
+        ptx::cluster_wait_acquire();  // both CTAs finished reading E (previous line's stage C)
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+            const uint32_t off = (uint32_t)(((k & 15) * kL14cP1 + t) * 8);
+            if ((uint32_t)(k >> 4) == r)
+                E[(k & 15) * kL14cP1 + t] = v[k];
+            else
+                ptx::st_cluster_f2(e_peer + off, v[k]);
+        }
+        ptx::cluster_arrive_release();
+        ptx::cluster_wait_acquire();  // E1 complete in both CTAs
+        // ---- B: (k1l, t1), values over t2
+        const int k1l = j & 15, t1 = j >> 4;
+#pragma unroll
+        for (int m = 0; m < 32; ++m) v[m] = E[k1l * kL14cP1 + t1 + 16 * m];
+        dft<32>(v);
+        {
+            float2 bB[5];  // W_512^{t1 2^i}
+#pragma unroll
+            for (int i = 0; i < 5; ++i) bB[i] = __ldg(tw + (((t1 << i) << 5) & (kTwN - 1)));
+            apply_pow32(v, bB);
+        }
+        __syncthreads();  // every thread has read E1
+#pragma unroll
+        for (int k = 0; k < 32; ++k) E[(k * 16 + t1) * 16 + k1l] = v[k];  // E2[k2b][t1][k1l]
+        __syncthreads();
+        // ---- C: k2b in {2 (j >> 4), 2 (j >> 4) + 1}, length-16 DFT over t1
+        float2* dst = p.out + g * p.lout.hi;
+        const int k1 = 16 * (int)r + k1l;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int k2b = 2 * (j >> 4) + h;
+            float2 u[16];
+#pragma unroll
+            for (int q = 0; q < 16; ++q) u[q] = E[(k2b * 16 + q) * 16 + k1l];
+            dft<16>(u);
+#pragma unroll
+            for (int c = 0; c < 16; ++c) {
+                float2 o = u[c];
+                if (p.conj_out) o.y = -o.y;
+                if (p.scale != 1.0f) o = __fmul2_rn(o, bc2(p.scale));
+                const int k = k1 + 32 * k2b + 1024 * c;
+                if constexpr (!OUT_GENERIC) {
+                    dst[k] = o;
+                } else {
+                    const int out_kmask = (1 << p.lout.kb_shift) - 1;
+                    if (p.peer_out)
+                        p.peer[k >> p.lout.kb_shift][g * p.lout.hi + (int64_t)(k & out_kmask) * p.lout.es] = o;
+                    else
+                        dst[(int64_t)(k & out_kmask) * p.lout.es + (int64_t)(k >> p.lout.kb_shift) * p.lout.bs] = o;
+                }
+            }
+        }
+        ptx::cluster_arrive_release();  // this CTA is done reading E for this line
+    }
+    ptx::cluster_wait_acquire();  // no peer writes into E after this CTA exits
+}
+
+template <bool OG, int CPS>
+static fb_status launch_row16384c_cps(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    static DevOnce once;
+    const int dev = DevOnce::dev();
+    if (!once.done(dev)) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(fft_row16384c_kernel<OG, CPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)kL14cSmem));
+        once.set(dev);
+    }
+    int64_t clusters = (int64_t)st->sm_count * CPS / 2;
+    if (clusters > p.nlines) clusters = p.nlines;
+    return launch_pdl(fft_row16384c_kernel<OG, CPS>, dim3((unsigned)(2 * clusters)), dim3(kL14cThreads), kL14cSmem,
+                      s, p, (const float2*)st->twiddles);
+}
+// CTAs per SM (knob FB_FFT_ROW16K_CPS): 2 (128 registers) or 3 (85 registers)
+template <bool OG>
+static fb_status launch_row16384c(const FftPass& p, const DeviceState* st, cudaStream_t s) {
+    return knobs().fft_row16k_cps == 3 ? launch_row16384c_cps<OG, 3>(p, st, s) : launch_row16384c_cps<OG, 2>(p, st, s);
+}
+
 template <bool OG>
 static fb_status launch_longrow(const FftPass& p, const DeviceState* st, cudaStream_t s) {
     using G = LineGeom<14>;
@@ -1667,6 +1804,9 @@ fb_status launch_pass_L(const FftPass& p, const DeviceState* st, cudaStream_t s)
         if (longrow_eligible(p)) {
             // the 32 x 32 x 16 four-step kernel, plain or per-peer outputs (knob FB_FFT_ROW16K=0:
             // the radix-16 half-line-streaming kernel)
+            if (knobs().fft_row16k == 2)  // each line over a CTA pair (DSMEM exchange)
+                return p.lout.kb_shift >= 14 && !p.peer_out ? launch_row16384c<false>(p, st, s)
+                                                            : launch_row16384c<true>(p, st, s);
             if (knobs().fft_row16k)
                 return p.lout.kb_shift >= 14 && !p.peer_out ? launch_row16384<false>(p, st, s)
                                                             : launch_row16384<true>(p, st, s);

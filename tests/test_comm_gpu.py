@@ -137,6 +137,24 @@ def test_fused_model_all_P_bitwise(env, n0, n1):
             assert torch.equal(z, z1), P
 
 
+@pytest.mark.parametrize("row16k", ["1", "2"])
+def test_fused_model_16384_rows_bitwise(env, row16k, monkeypatch):
+    """16384-long rows through the per-peer output map (the slab transpose's row pass in the
+    one-CTA-per-line and the CTA-pair kernels): P = 2, 4, 8 assemble to P = 1 bit for bit."""
+    fb, _ = env
+    monkeypatch.setenv("FB_FFT_ROW16K", row16k)
+    n0, n1 = 64, 16384
+    x = torch.from_numpy(synth.complex_field(n0, n1)).cuda()
+    ys = {}
+    for P in (1, 2, 4, 8):
+        y = torch.empty(n0 * n1, dtype=torch.complex64, device="cuda")
+        fb.fb_fft2d_slab_model(P, x, y, n0, n1)
+        ys[P] = _assemble(y, P, n0, n1)
+    torch.cuda.synchronize()
+    for P in (2, 4, 8):
+        assert torch.equal(ys[P], ys[1]), P
+
+
 def test_fused_model_vs_oracle(env):
     fb, _ = env
     n0, n1, P = 512, 256, 4

@@ -423,6 +423,26 @@ def test_non_power_of_two_closed_forms(fb):
     assert np.abs(yd - ref).max() < 1e-5
 
 
+@pytest.mark.parametrize("inverse", [False, True])
+def test_row16384_cluster_kernel_bitwise(fb, inverse, monkeypatch):
+    """FB_FFT_ROW16K=2: each 16384-long line split over a CTA pair (stage-A outputs exchanged
+    through distributed shared memory, two or three half-line CTAs per SM) runs the per-element
+    operations of the one-CTA-per-line kernel, so 1D rows (conj/scale of the inverse included)
+    and a 2D transform with 16384-long rows are bitwise equal to it."""
+    n0, n1 = 300, 16384
+    x = torch.from_numpy(synth.complex_field(n0, n1)).cuda()
+    y1 = fb.fft1d(x, inverse=inverse)
+    x2 = torch.from_numpy(synth.complex_field(64, 16384)).cuda()
+    z1 = fb.fft2d(x2, inverse=inverse)
+    monkeypatch.setenv("FB_FFT_ROW16K", "2")
+    y2 = fb.fft1d(x, inverse=inverse)
+    z2 = fb.fft2d(x2, inverse=inverse)
+    monkeypatch.setenv("FB_FFT_ROW16K_CPS", "3")
+    y3 = fb.fft1d(x, inverse=inverse)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2) and torch.equal(z1, z2) and torch.equal(y1, y3)
+
+
 def test_longrow_kernel_matches_plain_kernel(fb, monkeypatch):
     """16384-long rows: the radix-16 persistent half-prefetching kernel (FB_FFT_ROW16K=0) and the
     plain kernel run the same per-line arithmetic (bit for bit); the default 32 x 32 x 16

@@ -15,7 +15,7 @@ ki, mi, vi, ui = h.index("Kernel Name"), h.index("Metric Name"), h.index("Metric
 scale = {"ns": 1.0, "nsecond": 1.0, "us": 1e3, "usecond": 1e3, "ms": 1e6, "msecond": 1e6}
 agg = collections.OrderedDict()
 ours = []
-OURS = ("fb::", "lu::", "tf32::", "f64::", "pair::", "fft_pass", "gemm_", "lu_", "split_", "lsa_")
+OURS = ("fb::", "lu::", "tf32::", "f64::", "pair::", "fft_", "gemm_", "lu_", "split_", "lsa_", "bs_", "rfft_", "scale_kernel")
 for r in rows[start + 1:]:
     if len(r) <= max(ki, mi, vi) or r[mi] != "gpu__time_duration.sum":
         continue
