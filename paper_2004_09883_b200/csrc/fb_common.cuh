@@ -63,6 +63,7 @@ struct Knobs {
     int fft_no_tma_row = 0, fft_col_nb = 0, fft_row_nb = 0, fft_no_tma = 0, fft_longrow = 1, fft_pair_tma = 1;
     int fft_no_pdl = 0, fft_debug = 0, fft_sub = 0;  // FB_FFT_SUB: 0 auto, 1 / 3 forced
     int fft_sub_ilv = 0, fft_col32 = 1, fft_row16k = 1, fft_row16k_cps = 2;
+    int fft_small = 16;  // 256 x 256 as one cluster kernel: cluster size 16 (8), 0 = two-pass path
     // multi-GPU (fb_comm.cu)
     int slab_fused = 1;
     int64_t rowblock_panel = 4096;
@@ -178,6 +179,9 @@ fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inve
 // Non-power-of-two sizes (fb_bluestein.cu): each dimension a power of two <= 16384 or any
 // length <= 8192 (Bluestein chirp-z over power-of-two passes)
 bool fft_size_ok(int64_t n);
+// 256 x 256 in one thread-block-cluster kernel (fb_fft_small.cu)
+bool fft_small_eligible(int64_t n0, int64_t n1);
+fb_status fft2d_small(const float2* x, float2* y, bool inverse, float scale, const DeviceState* st, cudaStream_t s);
 size_t bluestein_ws_bytes(int64_t n0, int64_t n1);
 fb_status fft2d_bluestein(const void* x, void* y, int64_t n0, int64_t n1, bool inverse, void* ws, size_t ws_bytes,
                           const DeviceState* st, cudaStream_t s, bool unscaled);

@@ -164,6 +164,8 @@ fb_status fft2d_device(const void* x, void* y, int64_t n0, int64_t n1, bool inve
                        size_t ws_bytes, const DeviceState* st, cudaStream_t s, bool unscaled) {
     if (!is_pow2(n0) || !is_pow2(n1)) return fft2d_bluestein(x, y, n0, n1, inverse, ws, ws_bytes, st, s, unscaled);
     const float scale = (inverse && !unscaled) ? 1.0f / (float)((double)n0 * (double)n1) : 1.0f;
+    if (fft_small_eligible(n0, n1) && aligned16(x) && aligned16(y))
+        return fft2d_small((const float2*)x, (float2*)y, inverse, scale, st, s);
     if (use_pair_plan(n0, n1) && aligned16(x) && aligned16(y) && aligned16(ws)) {
         if (ws_bytes < fft2d_ws_bytes(n0, n1)) {
             set_error("workspace too small");

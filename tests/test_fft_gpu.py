@@ -63,6 +63,31 @@ def test_full_oracle(fb, n0, n1):
     assert oracle.rel_l2(z, oracle.dft2d(y.astype(np.complex64), inverse=True)) < 5e-7
 
 
+@pytest.mark.parametrize("small", ["8", "16", "0"])
+def test_fft256_cluster_kernel_vs_oracle(fb, small, monkeypatch):
+    """configs[0] as one thread-block-cluster kernel (fb_fft_small.cu; FB_FFT_SMALL = cluster size
+    8 or 16, 0 = the two-pass path): forward against the full oracle, inverse round trip, in place
+    (x == y), bitwise deterministic, and a single tone lands in one bin."""
+    monkeypatch.setenv("FB_FFT_SMALL", small)
+    xh = synth.complex_field(256, 256)
+    x = torch.from_numpy(xh).cuda()
+    y = fb.fft2d(x)
+    y2 = fb.fft2d(x)
+    z = fb.fft2d(y, inverse=True)
+    w = x.clone()
+    fb.fft2d(w, out=w)
+    torch.cuda.synchronize()
+    assert torch.equal(y, y2) and torch.equal(w, y)
+    assert oracle.rel_l2(y.cpu().numpy(), oracle.dft2d(xh)) < 5e-7
+    assert oracle.rel_l2(z.cpu().numpy(), xh) < 5e-7
+    i0, i1 = np.meshgrid(np.arange(256), np.arange(256), indexing="ij")
+    tone = np.exp(2j * np.pi * (3 * i0 + 250 * i1) / 256).astype(np.complex64)
+    yt = fb.fft2d(torch.from_numpy(tone).cuda()).cpu().numpy()
+    ref = np.zeros((256, 256), np.complex128)
+    ref[3, 250] = 65536
+    assert np.abs(yt - ref).max() < 65536 * 1e-5
+
+
 def test_256_forward_inverse_config0(fb):
     """BASELINE configs[0]: 256x256 fp32, single forward + inverse."""
     x = synth.complex_field(256, 256)
