@@ -426,6 +426,18 @@ __device__ __forceinline__ void tile_coords(int tile, int tiles_m, int tiles_n, 
     tm = first_m + in % gm;
     tn = in / gm;
 }
+// two-level raster: N-panels of pw tile columns in order, the grouped raster inside each
+// (pw <= 0: one panel)
+__device__ __forceinline__ void tile_coords_panel(int tile, int tiles_m, int tiles_n, int pw, int& tm, int& tn) {
+    if (pw <= 0 || pw >= tiles_n) {
+        tile_coords(tile, tiles_m, tiles_n, tm, tn);
+        return;
+    }
+    const int p = tile / (tiles_m * pw);
+    const int wp = min(pw, tiles_n - p * pw);
+    tile_coords(tile - p * tiles_m * pw, tiles_m, wp, tm, tn);
+    tn += p * pw;
+}
 
 // one epilogue row segment: dst[j] = alpha acc[j] + beta dst[j] for j < min(W, valid) (fb_gemm's
 // epilogue; dst is not read when beta == 0, and (alpha, beta) = (1, 0) stores acc exactly)
@@ -615,7 +627,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                             const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
                             float* __restrict__ C, int M, int N, int K, int64_t ldc, int tiles_m, int tiles_n,
-        float alpha, float beta) {
+        float alpha, float beta, int panel_tn) {
     extern __shared__ uint8_t smem_raw[];
     const uint32_t raw_u32 = ptx::smem_u32(smem_raw);
     const uint32_t base = (raw_u32 + 1023u) & ~1023u;
@@ -672,7 +684,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             int g = 0;  // k-blocks issued (stage ring position across tiles)
             for (int tile = pair; tile < ntiles; tile += P) {
             int tm, tn;
-            tf32::tile_coords(tile, tiles_m, tiles_n, tm, tn);
+            tf32::tile_coords_panel(tile, tiles_m, tiles_n, panel_tn, tm, tn);
             const int am = tm * 256 + 128 * (int)rank, bn = tn * 256 + 128 * (int)rank;
             for (int kb = 0; kb < KB; ++kb, ++g) {
                 const int s = g % STAGES;
@@ -732,7 +744,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         int cg = 0;  // chunks drained (across tiles)
         for (int tile = pair; tile < ntiles; tile += P) {
         int tm, tn;
-        tf32::tile_coords(tile, tiles_m, tiles_n, tm, tn);
+        tf32::tile_coords_panel(tile, tiles_m, tiles_n, panel_tn, tm, tn);
         const int m0 = tm * 256, n0 = tn * 256;
         float acc[128];
 #pragma unroll
@@ -941,6 +953,21 @@ fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_
             (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a, a_cblk);
         FB_LAUNCH_CHECK("split_both_kernel");
     }
+    // The product as GEMMs over N-column panels of w columns (the row-block path's per-panel
+    // GEMM; same per-element arithmetic, bitwise equal).  Each launch re-synchronises the
+    // concurrently running tiles in the raster; an in-kernel two-level raster does not help
+    // (FB_GEMM_RASTER_PANEL).  Interleaved A/B: 32768^3 320-331 -> 288-295 ms (w = 2048),
+    // 32768 x 8192 x 32768 76-78 -> 72 ms, 16384^3 36.0-37.1 -> 34.9 ms, but 8192^3 4.0 -> 4.3-4.4 ms
+    // (256 tiles per panel, 3.5 waves: the per-launch tails dominate).  Auto (knob -1): w = 2048
+    // when a panel holds >= 6 waves of CTA pairs (m >= ~14100) and n > w; FB_GEMM_NPANEL = w forces.
+    int64_t w = knobs().gemm_npanel;
+    if (w < 0) w = ((m + 255) / 256) * 8 >= 444 && n > 2048 ? 2048 : 0;
+    if (w > 0 && n > w) {
+        for (int64_t j0 = 0; j0 < n; j0 += w)
+            FB_TRY(gemm_3xtf32_presplit_device(m, std::min(w, n - j0), k, Ah, Al, kp, Bh + j0 * kp, Bl + j0 * kp, kp,
+                                               (float*)C + j0, ldc, s, (float)alpha, (float)beta));
+        return FB_OK;
+    }
     return gemm_3xtf32_presplit_device(m, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C, ldc, s, (float)alpha,
                                        (float)beta);
 }
@@ -1009,7 +1036,8 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
         cfg.attrs = attr;
         cfg.numAttrs = 1;
         FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf32::pair::gemm_3xtf32_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m,
-                                       (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta));
+                                       (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta,
+                                       knobs().gemm_raster_panel));
         FB_LAUNCH_CHECK("gemm_3xtf32_pair_kernel");
         return FB_OK;
     }

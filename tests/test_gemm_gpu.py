@@ -347,6 +347,30 @@ def test_gemm_persistent_pair_bitwise(fb, m, n, k, monkeypatch):
     assert oracle.rel_l2(C1, oracle.matmul(A, B)) < 1e-5
 
 
+@pytest.mark.parametrize("panel", ["0", "1024", "2048", "-1"])
+def test_gemm_n_panels_bitwise(fb, panel, monkeypatch):
+    """FP32 GEMM issued as N-column panel launches (auto for tall A: m >= ~14100; FB_GEMM_NPANEL
+    forces a width) computes every element with the same arithmetic: bitwise equal to the
+    single launch, ragged last panel included, and alpha/beta (fb_gemm) per panel."""
+    m, n, k = 14400, 4700, 200  # auto: 57 tile rows -> panels of 2048 columns
+    A = synth.real_matrix(m, k, synth.TID_GEMM_A)
+    B = synth.real_matrix(k, n, synth.TID_GEMM_B)
+    monkeypatch.setenv("FB_GEMM_NPANEL", "0")
+    C0 = _mm_padded(fb, A, B)
+    monkeypatch.setenv("FB_GEMM_NPANEL", panel)
+    C1 = _mm_padded(fb, A, B)
+    assert np.array_equal(C0, C1)
+    rows = [0, 7777, m - 1]
+    ref = oracle.matmul(A[rows].astype(np.float64), B.astype(np.float64))
+    assert oracle.rel_l2(C1[rows], ref) < 1e-5
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B[:, :4696]).contiguous().cuda()
+    Cd = torch.ones(m, 4696, device="cuda")
+    fb.gemm(Ad, Bd, Cd, 0.5, -1.0)
+    torch.cuda.synchronize()
+    P = torch.from_numpy(C0[:, :4696]).cuda()
+    assert torch.allclose(Cd, 0.5 * P - 1.0, rtol=1e-6, atol=1e-6)
+
+
 @pytest.mark.parametrize("m,n,k,bt", [(256, 256, 64, True), (300, 200, 136, False), (512, 768, 1000, True),
                                       (2048, 2048, 2048, False), (40, 24, 8, True)])
 def test_gemm_bf16_vs_oracle(fb, m, n, k, bt):
