@@ -40,7 +40,7 @@ extern "C" {
 typedef enum {
     FB_OK = 0,
     FB_ERR_INVALID_VALUE = 1,    /* null pointer, bad flag, partial overlap, n % P != 0 ... */
-    FB_ERR_UNSUPPORTED_SIZE = 2, /* FFT length not a power of two or > 2^14 */
+    FB_ERR_UNSUPPORTED_SIZE = 2, /* FFT length > 2^14, or not a power of two and > 8192 */
     FB_ERR_MISALIGNED = 3,       /* pointer not 16-byte aligned / leading dim breaks TMA rule */
     FB_ERR_WORKSPACE = 4,        /* workspace pointer null or smaller than *_workspace_bytes */
     FB_ERR_NOT_INITIALIZED = 5,  /* fb_comm_* on a null or destroyed communicator */
@@ -73,14 +73,18 @@ fb_status fb_init(int device);
 /* ------------------------------------------------------------------ Fourier block
  * Y = DFT2(X) over an n0 x n1 complex64 array (n0 rows, n1 contiguous columns):
  *   Y[k0,k1] = sum_{t0,t1} X[t0,t1] exp(-2 pi i (k0 t0/n0 + k1 t1/n1))      (unscaled)
- * fb_ifft2d: sign +1 and the factor 1/(n0 n1) (exact: a power of two).
+ * fb_ifft2d: sign +1 and the factor 1/(n0 n1) (exact when n0 n1 is a power of two, else the
+ * FP32 rounding of the FP64 reciprocal).
  * Reading R1 (sign -1 forward, cuFFT/numpy convention), R2 (inverse scaled), R3 (layout),
- * R4 (sizes): n0, n1 powers of two, 1 <= n <= 16384.
+ * R4 / R22 (sizes): each of n0, n1 a power of two <= 16384, or any other length <= 8192
+ * (lengths that factor into 2, 3, 5, 7: mixed-radix Stockham lines; others: Bluestein's
+ * chirp-z over power-of-two passes).
  * x and y: device pointers, 16-byte aligned, n0*n1*8 bytes each; x == y (in place) is
  * allowed, partial overlap is FB_ERR_INVALID_VALUE.
  * ws: device workspace of fb_fft2d_workspace_bytes(n0, n1) bytes (may be NULL when that
- * is 0: n0 < 512 or n0 == 4096; the 2 x n0/2 column split for 512 <= n0 <= 2048 and the
- * four-step split for n0 > 4096 use n0*n1*8 bytes).  Not read before written; contents
+ * is 0: power-of-two n0 < 512 or n0 == 4096; the 2 x n0/2 column split for 512 <= n0 <= 2048
+ * and the four-step split for n0 > 4096 use n0*n1*8 bytes; other sizes a transpose buffer,
+ * the convolution lines and the chirp / twiddle tables).  Not read before written; contents
  * undefined afterwards.
  * Accuracy (north_star): rel-L2 <= 1e-5 * log2(n0 n1) vs the exact DFT; internal gate
  * 5e-7 (reading R6). */

@@ -411,12 +411,18 @@ def test_radix32_column_pass_vs_oracle(fb, n0, n1, monkeypatch):
     assert oracle.rel_l2(outs["1"], outs["0"]) < 5e-7
 
 
+@pytest.mark.parametrize("mixed", ["1", "0", "2"])
 @pytest.mark.parametrize("n0,n1", [(3, 5), (7, 64), (1, 999), (1000, 1), (100, 36), (360, 480), (12, 8191),
-                                   (2048, 1000), (625, 243)])
-def test_non_power_of_two_vs_oracle(fb, n0, n1):
-    """sizes that are not powers of two (Bluestein chirp-z over the power-of-two
-    passes, fb_bluestein.cu) against the full oracle, forward and inverse, within the north_star
-    bar 1e-5 log2(n0 n1); in place equals out of place."""
+                                   (2048, 1000), (625, 243), (2401, 6), (10, 6561), (3125, 5), (14, 8000),
+                                   (4200, 6), (6, 4200), (1000, 24)])
+def test_non_power_of_two_vs_oracle(fb, n0, n1, mixed, monkeypatch):
+    """sizes that are not powers of two against the full oracle, forward and
+    inverse, within the north_star bar 1e-5 log2(n0 n1); in place equals out of place.  Lines
+    whose length factors into 2, 3, 5, 7 run the mixed-radix Stockham kernel (FB_FFT_MIXED=1,
+    radix 8/4/2/3/5/7 stages; =2 also runs the columns in place, C at a time), the others
+    (999 = 27 * 37, the prime 8191) and every line with FB_FFT_MIXED=0 Bluestein's chirp-z over
+    the power-of-two passes (fb_bluestein.cu)."""
+    monkeypatch.setenv("FB_FFT_MIXED", mixed)
     x = synth.complex_field(n0, n1, tensor_id=7)
     ref = oracle.dft2d(x)
     y = _run(fb, x)
@@ -427,6 +433,24 @@ def test_non_power_of_two_vs_oracle(fb, n0, n1):
     assert e < _bar(n0, n1) and ei < _bar(n0, n1), (e, ei)
     assert e < 2e-6  # the measured level (FP32 chirp-z): well inside the bar
     assert np.array_equal(_run(fb, x, inplace=True), y)
+
+
+@pytest.mark.parametrize("mixed", ["1", "0", "2"])
+def test_non_power_of_two_square_tone(fb, mixed, monkeypatch):
+    """4200 x 4200 (2^3 3 5^2 7): square with columns longer than 4096, one column per CTA in the
+    mixed-radix kernel; a single tone must land in one bin with the rest at rounding level."""
+    monkeypatch.setenv("FB_FFT_MIXED", mixed)
+    n = 4200
+    f0, f1 = 1234, 4001
+    i0 = torch.arange(n, dtype=torch.float64, device="cuda")[:, None]
+    i1 = torch.arange(n, dtype=torch.float64, device="cuda")[None, :]
+    ph = 2 * np.pi * (torch.remainder(f0 * i0, n) / n + torch.remainder(f1 * i1, n) / n)
+    tone = torch.polar(torch.ones_like(ph), ph).to(torch.complex64)
+    y = fb.fft2d(tone)
+    peak = complex(y[f0, f1].item())
+    y[f0, f1] = 0
+    rest = float(y.abs().max().item())
+    assert abs(peak - n * n) < 1e-4 * n * n and rest < 1e-4 * n * n, (peak, rest)
 
 
 def test_non_power_of_two_closed_forms(fb):
