@@ -115,28 +115,13 @@ __global__ void __launch_bounds__(Geo<CL>::THREADS, 1)
 }
 }  // namespace small
 
-bool fft_small_eligible(int64_t n0, int64_t n1) {
-    return n0 == small::N && n1 == small::N && knobs().fft_small != 0;
-}
-
 template <int CL>
-static fb_status launch_small(const float2* x, float2* y, bool inverse, float scale, const DeviceState* st,
-                              cudaStream_t s) {
-    using G = small::Geo<CL>;
-    auto kern = small::fft256_cluster_kernel<CL>;
-    static DevOnce once;
-    const int dev = DevOnce::dev();
-    if (!once.done(dev)) {
-        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G::SMEM));
-        if (CL > 8) FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-        once.set(dev);
-    }
-    cudaLaunchConfig_t cfg = {};
+static void small_cfg(cudaLaunchConfig_t& cfg, cudaLaunchAttribute* at, cudaStream_t s) {
+    cfg = {};
     cfg.gridDim = dim3(CL);
-    cfg.blockDim = dim3(G::THREADS);
-    cfg.dynamicSmemBytes = G::SMEM;
+    cfg.blockDim = dim3(small::Geo<CL>::THREADS);
+    cfg.dynamicSmemBytes = small::Geo<CL>::SMEM;
     cfg.stream = s;
-    cudaLaunchAttribute at[2];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = CL;
     at[0].val.clusterDim.y = 1;
@@ -145,7 +130,49 @@ static fb_status launch_small(const float2* x, float2* y, bool inverse, float sc
     at[1].val.programmaticStreamSerializationAllowed = 1;
     cfg.attrs = at;
     cfg.numAttrs = 2;
-    FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, x, y, (const float2*)st->twiddles, inverse ? 1 : 0, scale));
+}
+
+template <int CL>
+static fb_status prepare_small(int dev, bool* schedulable) {
+    auto kern = small::fft256_cluster_kernel<CL>;
+    static DevOnce once;
+    static std::atomic<int> ok[64];
+    if (!once.done(dev)) {
+        FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)small::Geo<CL>::SMEM));
+        if (CL > 8) FB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+        // a 16-CTA cluster needs 16 SMs of one GPC free at once: if the device (a partitioned GPU)
+        // cannot place it, fft2d_device keeps the two-pass path for this size
+        cudaLaunchConfig_t cfg;
+        cudaLaunchAttribute at[2];
+        small_cfg<CL>(cfg, at, 0);
+        int nc = 0;
+        if (cudaOccupancyMaxActiveClusters(&nc, kern, &cfg) != cudaSuccess) {
+            cudaGetLastError();
+            nc = 0;
+        }
+        ok[dev & 63].store(nc > 0 ? 1 : 0);
+        once.set(dev);
+    }
+    *schedulable = ok[dev & 63].load() != 0;
+    return FB_OK;
+}
+
+bool fft_small_eligible(int64_t n0, int64_t n1) {
+    if (n0 != small::N || n1 != small::N || knobs().fft_small == 0) return false;
+    bool sched = false;
+    const int dev = DevOnce::dev();
+    const fb_status rc = knobs().fft_small == 8 ? prepare_small<8>(dev, &sched) : prepare_small<16>(dev, &sched);
+    return rc == FB_OK && sched;
+}
+
+template <int CL>
+static fb_status launch_small(const float2* x, float2* y, bool inverse, float scale, const DeviceState* st,
+                              cudaStream_t s) {
+    cudaLaunchConfig_t cfg;
+    cudaLaunchAttribute at[2];
+    small_cfg<CL>(cfg, at, s);
+    FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, small::fft256_cluster_kernel<CL>, x, y, (const float2*)st->twiddles,
+                                   inverse ? 1 : 0, scale));
     FB_LAUNCH_CHECK("fft256_cluster_kernel");
     return FB_OK;
 }
