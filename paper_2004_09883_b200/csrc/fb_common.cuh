@@ -67,7 +67,7 @@ struct Knobs {
     int fft_small = 16;  // 256 x 256 as one cluster kernel: cluster size 16 (8), 0 = two-pass path
     // multi-GPU (fb_comm.cu)
     int slab_fused = 1;
-    int64_t rowblock_panel = 4096;
+    int64_t rowblock_panel = 2048;  // same width as fb_matmul's N-panel launches (32768^3 at world 1: 307 -> 301 ms)
     // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
     int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
     int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 0, gemm_lo_overlap = 0, gemm_persist = 0;
