@@ -50,6 +50,7 @@ static Knobs read_knobs() {
     k.fft_row16k_cps = env_int("FB_FFT_ROW16K_CPS", k.fft_row16k_cps);
     k.fft_small = env_int("FB_FFT_SMALL", k.fft_small);
     k.fft_mixed = env_int("FB_FFT_MIXED", k.fft_mixed);
+    k.fft_mr_small = env_int("FB_FFT_MR_SMALL", k.fft_mr_small);
     k.slab_fused = env_int("FB_SLAB_FUSED", k.slab_fused);
     const char* pk = getenv("FB_ROWBLOCK_PANEL");
     if (pk && pk[0]) k.rowblock_panel = atoll(pk);

@@ -356,8 +356,10 @@ static fb_status mixed_lines(const float2* x, float2* y, int64_t batch, int64_t 
         mr_lines_kernel<true><<<(unsigned)ctas, 256, smem, s>>>(x, y, (int)n, C, ncols, ncols, mr_plan(n), W,
                                                                inverse ? 1 : 0, inverse ? 1 : 0, scale);
     else
-        mr_lines_kernel<false><<<(unsigned)ctas, 256, smem, s>>>(x, y, (int)n, 1, n, batch, mr_plan(n), W,
-                                                                inverse ? 1 : 0, inverse ? 1 : 0, scale);
+        // rows: 128 threads for n <= 1024 (a radix-8 stage has <= 128 butterflies; 256-thread CTAs
+        // were register-limited to 4 per SM, 1.69 waves at 1000^2), else 256
+        mr_lines_kernel<false><<<(unsigned)ctas, n <= knobs().fft_mr_small ? 128 : 256, smem, s>>>(
+            x, y, (int)n, 1, n, batch, mr_plan(n), W, inverse ? 1 : 0, inverse ? 1 : 0, scale);
     FB_LAUNCH_CHECK("mr_lines_kernel");
     return FB_OK;
 }
