@@ -71,7 +71,7 @@ struct Knobs {
     // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
     int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
     int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 0, gemm_lo_overlap = 0, gemm_persist = 0;
-    int gemm_npanel = -1, gemm_raster_panel = 0;  // -1: auto N-panels (fb_gemm.cu)
+    int gemm_npanel = -1, gemm_raster_panel = 0, gemm_nt = 0;  // -1: auto N-panels (fb_gemm.cu)
     int bf16_persist = 1;  // 8192^3 0.820 -> 0.790 ms, 4096^3 0.145 -> 0.124 ms (interleaved A/B)
     // LU (fb_lu.cu)
     int lu_tma = 1, lu_debug = 0, lu_rank_simt = 1, lu_serial = 0, lu_lookahead = 1, lu_graph = 1;

@@ -623,6 +623,9 @@ constexpr uint32_t ACC_COLS = 256;                        // N of the pair MMA
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;              // double-buffered accumulator
 constexpr int KP_BLOCKS = 4;
 
+// NT: N of the pair tile (256, or 240 so that e.g. 2048 columns make 9 tiles and 2048^2 fills 72 of
+// the 74 CTA pairs in one wave); each CTA stages NT / 2 rows of B^T
+template <int NT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     gemm_3xtf32_pair_kernel(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
                             const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
@@ -685,12 +688,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
             for (int tile = pair; tile < ntiles; tile += P) {
             int tm, tn;
             tf32::tile_coords_panel(tile, tiles_m, tiles_n, panel_tn, tm, tn);
-            const int am = tm * 256 + 128 * (int)rank, bn = tn * 256 + 128 * (int)rank;
+            const int am = tm * 256 + 128 * (int)rank, bn = tn * NT + (NT / 2) * (int)rank;
             for (int kb = 0; kb < KB; ++kb, ++g) {
                 const int s = g % STAGES;
                 const uint32_t ph = (uint32_t)(g / STAGES) & 1u;
                 ptx::mbar_wait(empty_bar(s), ph ^ 1u);
-                if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * STAGE_BYTES);
+                if (leader) ptx::mbar_arrive_expect_tx(full_bar(s), 2 * (2 * TILE_BYTES + 2 * (NT / 2) * BK * 4));
                 const uint32_t st = base + s * STAGE_BYTES;
                 const int kc = kb * BK;
                 ptx::tma_load_2d_pair(st, &tmAh, full_bar(s), kc, am);
@@ -703,7 +706,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
     } else if (warp == 1) {
         if (leader && lane == 0) {
             // ---------------- MMA issuer (leader CTA, single thread)
-            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+            const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) |
                                    ((uint32_t)(256 >> 4) << 24);
             int g = 0, cg = 0;  // k-blocks consumed, chunks issued (across tiles)
             for (int tile = pair; tile < ntiles; tile += P) {
@@ -745,34 +748,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(NUM_THREADS, 1)
         for (int tile = pair; tile < ntiles; tile += P) {
         int tm, tn;
         tf32::tile_coords_panel(tile, tiles_m, tiles_n, panel_tn, tm, tn);
-        const int m0 = tm * 256, n0 = tn * 256;
-        float acc[128];
+        constexpr int HALF = NT / 2;
+        const int m0 = tm * 256, n0 = tn * NT;
+        float acc[HALF];
 #pragma unroll
-        for (int j = 0; j < 128; ++j) acc[j] = 0.f;
+        for (int j = 0; j < HALF; ++j) acc[j] = 0.f;
         for (int c = 0; c < NCHUNK; ++c, ++cg) {
             const int buf = cg & 1;
             ptx::mbar_wait(tfull_bar(buf), (uint32_t)(cg >> 1) & 1u);
             ptx::tc_fence_after();
             const uint32_t taddr =
-                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC_COLS + h * 128);
+                tmem_base + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * ACC_COLS + h * HALF);
 #pragma unroll
-            for (int cb = 0; cb < 128; cb += 32) {
+            for (int cb = 0; cb + 32 <= HALF; cb += 32) {
                 uint32_t r[32];
                 ptx::tmem_ld_32x32b_x32(taddr + (uint32_t)cb, r);
                 ptx::tmem_ld_wait();
 #pragma unroll
                 for (int j = 0; j < 32; ++j) acc[cb + j] += __uint_as_float(r[j]);
             }
+            if constexpr (HALF % 32 >= 16) {  // NT = 240: columns 96..119 as x16 + x8
+                constexpr int cb = HALF / 32 * 32;
+                uint32_t r[16];
+                ptx::tmem_ld_32x32b_x16(taddr + (uint32_t)cb, r);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 16; ++j) acc[cb + j] += __uint_as_float(r[j]);
+            }
+            if constexpr (HALF % 16 == 8) {
+                constexpr int cb = HALF / 16 * 16;
+                uint32_t r[8];
+                ptx::tmem_ld_32x32b_x8(taddr + (uint32_t)cb, r);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int j = 0; j < 8; ++j) acc[cb + j] += __uint_as_float(r[j]);
+            }
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive_leader(tempty_bar(buf));
         }
         const int row = m0 + 128 * (int)rank + q * 32 + lane;
-        const int col0 = n0 + h * 128;
+        const int col0 = n0 + h * HALF;
         if (row < M) {
             float* dst = C + (int64_t)row * ldc + col0;
             const int valid = N - col0;
-            store_row<128>(dst, acc, valid, alpha, beta);
+            store_row<HALF>(dst, acc, valid, alpha, beta);
         }
         }
     }
@@ -1006,13 +1026,32 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
     if (!(attr_mask & (1 << (dev & 31)))) {
         FB_CUDA_TRY(cudaFuncSetAttribute(tf32::gemm_3xtf32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)tf32::SMEM));
-        FB_CUDA_TRY(cudaFuncSetAttribute(tf32::pair::gemm_3xtf32_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)tf32::pair::SMEM));
+        FB_CUDA_TRY(cudaFuncSetAttribute(tf32::pair::gemm_3xtf32_pair_kernel<256>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tf32::pair::SMEM));
+        FB_CUDA_TRY(cudaFuncSetAttribute(tf32::pair::gemm_3xtf32_pair_kernel<240>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tf32::pair::SMEM));
         attr_mask |= 1 << (dev & 31);
     }
     if (!one_cta) {
+        int sms = 148;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
         const int tiles_m = (int)((m + 255) / 256);
-        const int tiles_n = (int)((n + 255) / 256);
+        // N of the pair tile: 256, or 240 when that needs fewer (waves x tile width) -- e.g. 2048
+        // columns as 9 tiles of 240 put 2048^2 on 72 of the 74 CTA pairs in one wave (knob
+        // FB_GEMM_NT = 256 / 240 forces)
+        int nt = knobs().gemm_nt;
+        if (nt != 240 && nt != 256) {
+            auto cost = [&](int64_t t) {
+                const int64_t waves = ((int64_t)tiles_m * ((n + t - 1) / t) + sms / 2 - 1) / (sms / 2);
+                return waves * t;
+            };
+            nt = cost(240) < cost(256) ? 240 : 256;
+        }
+        if (nt == 240) {
+            FB_TRY(tf32::make_kmajor_map(&mBh, Bh, n, k, ldb, 120));
+            FB_TRY(tf32::make_kmajor_map(&mBl, Bl, n, k, ldb, 120));
+        }
+        const int tiles_n = (int)((n + nt - 1) / nt);
         const int64_t tiles = (int64_t)tiles_m * tiles_n;
         if (2 * tiles > INT32_MAX) {
             set_error("too many tiles");
@@ -1020,11 +1059,7 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
         }
         // persistent (knob FB_GEMM_PERSIST): one CTA pair per two SMs loops over the tiles
         int64_t pairs = tiles;
-        if (knobs().gemm_persist) {
-            int sms = 148;
-            cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-            pairs = std::min<int64_t>(tiles, sms / 2);
-        }
+        if (knobs().gemm_persist) pairs = std::min<int64_t>(tiles, sms / 2);
         cudaLaunchConfig_t cfg = {};
         cfg.gridDim = dim3((unsigned)(2 * pairs));
         cfg.blockDim = dim3(tf32::pair::NUM_THREADS);
@@ -1035,9 +1070,14 @@ fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const flo
         attr[0].val.programmaticStreamSerializationAllowed = 1;
         cfg.attrs = attr;
         cfg.numAttrs = 1;
-        FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf32::pair::gemm_3xtf32_pair_kernel, mAh, mAl, mBh, mBl, C, (int)m,
-                                       (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta,
-                                       knobs().gemm_raster_panel));
+        if (nt == 240)
+            FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf32::pair::gemm_3xtf32_pair_kernel<240>, mAh, mAl, mBh, mBl, C,
+                                           (int)m, (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta,
+                                           knobs().gemm_raster_panel));
+        else
+            FB_CUDA_TRY(cudaLaunchKernelEx(&cfg, tf32::pair::gemm_3xtf32_pair_kernel<256>, mAh, mAl, mBh, mBl, C,
+                                           (int)m, (int)n, (int)k, ldc, tiles_m, tiles_n, alpha, beta,
+                                           knobs().gemm_raster_panel));
         FB_LAUNCH_CHECK("gemm_3xtf32_pair_kernel");
         return FB_OK;
     }

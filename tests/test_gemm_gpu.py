@@ -347,6 +347,22 @@ def test_gemm_persistent_pair_bitwise(fb, m, n, k, monkeypatch):
     assert oracle.rel_l2(C1, oracle.matmul(A, B)) < 1e-5
 
 
+@pytest.mark.parametrize("m,n,k", [(2048, 2048, 512), (600, 1000, 300), (300, 250, 64), (512, 4096, 136)])
+def test_gemm_pair_tile_240_bitwise(fb, m, n, k, monkeypatch):
+    """FB_GEMM_NT=240: CTA-pair tiles 256 x 240 (MMA N = 240, each CTA stages 120 rows of B^T,
+    the epilogue drains 120 columns as 3 x32 + x16 + x8 TMEM loads).  A tile boundary does not
+    change any element's arithmetic, so the product is bitwise the 256-wide tiles' one (auto
+    picks 240 where it needs fewer waves x width, e.g. 2048^2)."""
+    A = synth.real_matrix(m, k, synth.TID_GEMM_A)
+    B = synth.real_matrix(k, n, synth.TID_GEMM_B)
+    monkeypatch.setenv("FB_GEMM_NT", "256")
+    C0 = _mm_padded(fb, A, B)
+    monkeypatch.setenv("FB_GEMM_NT", "240")
+    C1 = _mm_padded(fb, A, B)
+    assert np.array_equal(C0, C1)
+    assert oracle.rel_l2(C1, oracle.matmul(A, B)) < 1e-5
+
+
 @pytest.mark.parametrize("panel", ["0", "1024", "2048", "-1"])
 def test_gemm_n_panels_bitwise(fb, panel, monkeypatch):
     """FP32 GEMM issued as N-column panel launches (auto for tall A: m >= ~14100; FB_GEMM_NPANEL
