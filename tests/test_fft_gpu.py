@@ -414,7 +414,7 @@ def test_radix32_column_pass_vs_oracle(fb, n0, n1, monkeypatch):
 @pytest.mark.parametrize("mixed", ["1", "0", "2"])
 @pytest.mark.parametrize("n0,n1", [(3, 5), (7, 64), (1, 999), (1000, 1), (100, 36), (360, 480), (12, 8191),
                                    (2048, 1000), (625, 243), (2401, 6), (10, 6561), (3125, 5), (14, 8000),
-                                   (4200, 6), (6, 4200), (1000, 24)])
+                                   (4200, 6), (6, 4200), (1000, 24), (3, 7776)])
 def test_non_power_of_two_vs_oracle(fb, n0, n1, mixed, monkeypatch):
     """sizes that are not powers of two against the full oracle, forward and
     inverse, within the north_star bar 1e-5 log2(n0 n1); in place equals out of place.  Lines

@@ -182,6 +182,38 @@ def test_f32_k32768_sampled(fb):
     assert err < 1e-5
 
 
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_large_sampled_rows(fb, dt):
+    """4096^3 (FP32: 256 x 240 pair tiles in 4 waves; FP64: 4096 DMMA tiles) with full-mantissa
+    FP64 inputs where applicable: sampled full rows, including the first and last, against the
+    oracle's row function."""
+    n = 4096
+    mk = synth.real_matrix_f64 if dt == torch.float64 else synth.real_matrix
+    A, B = mk(n, n, synth.TID_GEMM_A), mk(n, n, synth.TID_GEMM_B)
+    C = _mm(fb, A, B)
+    rows = [0, 1, 255, 256, 2047, 4095]
+    err = oracle.rel_l2(C[rows], oracle.matmul_rows(A, B, rows))
+    assert err < (1e-5 if dt == torch.float32 else 1e-12), err
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.float64])
+def test_gemm_ex_transposed_large(fb, dt):
+    """fb_gemm with both operands transposed and alpha/beta at 2048^3 (FP32 picks 256 x 240
+    tiles): sampled rows against alpha op(A) op(B) + beta C0 formed by the oracle in FP64."""
+    n = 2048
+    mk = synth.real_matrix_f64 if dt == torch.float64 else synth.real_matrix
+    At, Bt, C0 = mk(n, n, synth.TID_GEMM_A), mk(n, n, synth.TID_GEMM_B), mk(n, n, synth.TID_NOISE)
+    C = torch.from_numpy(C0).to(dt).cuda()
+    fb.gemm(torch.from_numpy(At).to(dt).cuda(), torch.from_numpy(Bt).to(dt).cuda(), C, 1.5, -0.25, True, True)
+    torch.cuda.synchronize()
+    rows = [0, 777, 2047]
+    opA = np.ascontiguousarray(At.T).astype(np.float64)
+    opB = np.ascontiguousarray(Bt.T).astype(np.float64)
+    ref = 1.5 * oracle.matmul_rows(opA, opB, rows) - 0.25 * C0[rows].astype(np.float64)
+    err = oracle.rel_l2(C.cpu().numpy()[rows], ref)
+    assert err < (1e-5 if dt == torch.float32 else 1e-12), err
+
+
 def test_host_variant(fb):
     m, n, k = 300, 256, 128
     A = torch.from_numpy(synth.real_matrix(m, k, synth.TID_GEMM_A)).pin_memory()
