@@ -63,6 +63,7 @@ static Knobs read_knobs() {
     k.bf16_persist = env_int("FB_BF16_PERSIST", k.bf16_persist);
     k.gemm_npanel = env_int("FB_GEMM_NPANEL", k.gemm_npanel);
     k.gemm_nt = env_int("FB_GEMM_NT", k.gemm_nt);
+    k.gemm_ahi_raw = env_int("FB_GEMM_AHI_RAW", k.gemm_ahi_raw);
     k.gemm_raster_panel = env_int("FB_GEMM_RASTER_PANEL", k.gemm_raster_panel);
     k.gemm_fused = env_int("FB_GEMM_FUSED", k.gemm_fused);
     k.gemm_lo_prepass = env_int("FB_GEMM_LO_PREPASS", k.gemm_lo_prepass);

@@ -585,7 +585,14 @@ fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_
     const bool is_root = c->rank == root;
     FB_CUDA_TRY(cudaEventRecord(c->cev, s));  // the panel traffic starts after everything before the call
     FB_CUDA_TRY(cudaStreamWaitEvent(c->cstream, c->cev, 0));
-    if (dtype == FB_F32) FB_TRY(tf32_split_device(0, ml, k, (const float*)A_rows, lda, Ah, Al, L.kp, st, s));
+    // A's operands as fb_matmul forms them (raw hi + lo only by default), so the product is bitwise
+    const bool a_raw = dtype == FB_F32 && knobs().gemm_ahi_raw != 0;
+    if (dtype == FB_F32) {
+        if (a_raw)
+            FB_TRY(tf32_lo_device(ml, k, (const float*)A_rows, lda, Al, L.kp, s));
+        else
+            FB_TRY(tf32_split_device(0, ml, k, (const float*)A_rows, lda, Ah, Al, L.kp, st, s));
+    }
     int j = 0;
     for (int64_t j0 = 0; j0 < n; j0 += L.w, ++j) {
         const int64_t w = (n - j0) < L.w ? (n - j0) : L.w;
@@ -606,7 +613,8 @@ fb_status fb_matmul_rowblock(fb_comm* c, int dtype, int64_t m, int64_t n, int64_
             float* Bl = Bh + w * L.kp;
             FB_TRY(tf32_split_device(1, k, w, (const float*)panel, w, Bh, Bl, L.kp, st, s));
             FB_CUDA_TRY(cudaEventRecord(c->ev_used[sl], s));
-            FB_TRY(gemm_3xtf32_presplit_device(ml, w, k, Ah, Al, L.kp, Bh, Bl, L.kp, (float*)C_rows + j0, ldc, s));
+            FB_TRY(gemm_3xtf32_presplit_device(ml, w, k, a_raw ? (const float*)A_rows : Ah, Al, L.kp, Bh, Bl, L.kp,
+                                               (float*)C_rows + j0, ldc, s, 1.f, 0.f, a_raw ? lda : -1));
         } else {
             FB_TRY(gemm_device(FB_F64, ml, w, k, A_rows, lda, panel, w, (double*)C_rows + j0, ldc, nullptr, 0, st, s));
             FB_CUDA_TRY(cudaEventRecord(c->ev_used[sl], s));

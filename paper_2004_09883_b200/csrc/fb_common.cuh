@@ -71,7 +71,7 @@ struct Knobs {
     // GEMM (fb_gemm.cu, fb_gemm_bf16.cu)
     int f64_cfg = 0, gemm_split2 = 0, gemm_splitv = 0, gemm_split_pdl = 0, gemm_1cta = 0, bf16_cluster = 2;
     int gemm_fused = 0, gemm_lo_prepass = 1, gemm_streamk = 0, gemm_lo_overlap = 0, gemm_persist = 0;
-    int gemm_npanel = -1, gemm_raster_panel = 0, gemm_nt = 0;  // -1: auto N-panels (fb_gemm.cu)
+    int gemm_npanel = -1, gemm_raster_panel = 0, gemm_nt = 0, gemm_ahi_raw = 1;  // -1: auto N-panels (fb_gemm.cu)
     int bf16_persist = 1;  // 8192^3 0.820 -> 0.790 ms, 4096^3 0.145 -> 0.124 ms (interleaved A/B)
     // LU (fb_lu.cu)
     int lu_tma = 1, lu_debug = 0, lu_rank_simt = 1, lu_serial = 0, lu_lookahead = 1, lu_graph = 1;
@@ -208,7 +208,10 @@ fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_
 
 // G1: TF32 split (transpose=0: X[rows][cols] -> hi/lo [rows][ldo]; transpose=1: -> [cols][ldo])
 fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
-                            float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s);
+                            float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s, bool trunc_hi = false);
+// raw-hi mode of G1: lo = rna(x - trunc(x)) only (the raw X is the hi operand; reading R21)
+fb_status tf32_lo_device(int64_t rows, int64_t cols, const float* X, int64_t ldx, float* lo, int64_t ldo,
+                         cudaStream_t s);
 // G2-G4: C = Ah*Bh^T + Ah*Bl^T + Al*Bh^T with K-major split operands (A: m x k, B^T: n x k)
 // G1-G4 fused: C = A B (row-major FP32 A [m][k], B [k][n]), no workspace (fb_gemm_fused.cu)
 size_t gemm_3xtf32_fused_ws_bytes(int64_t m, int64_t n, int64_t k);
@@ -216,6 +219,7 @@ fb_status gemm_3xtf32_fused_device(int64_t m, int64_t n, int64_t k, const float*
                                    int64_t ldb, float* C, int64_t ldc, void* ws, size_t ws_bytes, cudaStream_t s);
 fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
                                       int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
-                                      int64_t ldc, cudaStream_t s, float alpha = 1.f, float beta = 0.f);
+                                      int64_t ldc, cudaStream_t s, float alpha = 1.f, float beta = 0.f,
+                                      int64_t lda_hi = -1);  // lda_hi: row pitch of Ah if != lda
 
 }  // namespace fb

@@ -220,9 +220,15 @@ __device__ __forceinline__ void split1(float x, float& h, float& l) {
     h = __uint_as_float(ptx::f32_to_tf32_rna(x));
     l = __uint_as_float(ptx::f32_to_tf32_rna(x - h));
 }
+// lo for a raw FP32 hi operand: the tensor core truncates an FP32 operand to TF32 (reading R21),
+// so hi = trunc(x) and lo = rna(x - trunc(x)) (x - trunc(x) is exact in FP32)
+__device__ __forceinline__ float lo_trunc(float x) {
+    return __uint_as_float(ptx::f32_to_tf32_rna(x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)));
+}
 
 // 2D grid: blockIdx.y = row block, x covers columns in float4 chunks (rows are 16-byte aligned:
 // ldx*4 and ldo*4 are multiples of 16 by the API contract).
+template <bool LO_ONLY = false>  // LO_ONLY: raw-hi mode, lo = rna(x - trunc(x)) only (hi unused)
 __global__ void split_rows_kernel(const float* __restrict__ X, int64_t rows, int64_t cols, int64_t ldx,
                                   float* __restrict__ hi, float* __restrict__ lo, int64_t ldo) {
     const int64_t c4 = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) * 4;
@@ -231,7 +237,15 @@ __global__ void split_rows_kernel(const float* __restrict__ X, int64_t rows, int
         const float* xr = X + r * ldx;
         float* hr = hi + r * ldo;
         float* lr = lo + r * ldo;
-        if (c4 + 4 <= cols) {
+        if constexpr (LO_ONLY) {
+            if (c4 + 4 <= cols) {
+                const float4 x = *reinterpret_cast<const float4*>(xr + c4);
+                *reinterpret_cast<float4*>(lr + c4) = make_float4(lo_trunc(x.x), lo_trunc(x.y), lo_trunc(x.z),
+                                                                  lo_trunc(x.w));
+            } else {
+                for (int64_t c = c4; c < cols; ++c) lr[c] = lo_trunc(xr[c]);
+            }
+        } else if (c4 + 4 <= cols) {
             const float4 x = *reinterpret_cast<const float4*>(xr + c4);
             float4 h, l;
             split1(x.x, h.x, l.x);
@@ -247,6 +261,9 @@ __global__ void split_rows_kernel(const float* __restrict__ X, int64_t rows, int
 }
 
 // B: [K][N] -> hi/lo [N][Kp] (transposed through a 32x33 smem tile so both sides coalesce).
+// TRUNC: raw-hi mode -- hi = trunc(x) (the value the tensor core uses for a raw FP32 operand),
+// lo = rna(x - trunc(x)), so a transposed operand gives the same product as the raw one
+template <bool TRUNC = false>
 __global__ void split_transpose_kernel(const float* __restrict__ X, int64_t rows, int64_t cols,
                                        int64_t ldx, float* __restrict__ hi, float* __restrict__ lo,
                                        int64_t ldo) {
@@ -257,8 +274,8 @@ __global__ void split_transpose_kernel(const float* __restrict__ X, int64_t rows
     for (int j = 0; j < 32; j += 8) {
         const int64_t r = r0 + ty + j, c = c0 + tx;
         float x = (r < rows && c < cols) ? X[r * ldx + c] : 0.f;
-        const uint32_t h = ptx::f32_to_tf32_rna(x);
-        const float hf = __uint_as_float(h);
+        const float hf = TRUNC ? __uint_as_float(__float_as_uint(x) & 0xFFFFE000u)
+                               : __uint_as_float(ptx::f32_to_tf32_rna(x));
         th[ty + j][tx] = hf;
         tl[ty + j][tx] = __uint_as_float(ptx::f32_to_tf32_rna(x - hf));
     }
@@ -336,7 +353,7 @@ __global__ void __launch_bounds__(256)
     split_both_wide_kernel(const float* __restrict__ A, int64_t m, int64_t k, int64_t lda, float* __restrict__ Ah,
                            float* __restrict__ Al, const float* __restrict__ B, int64_t n, int64_t ldb,
                            float* __restrict__ Bh, float* __restrict__ Bl, int64_t ldo, int64_t nblk_a,
-                           int pdl_trigger) {
+                           int pdl_trigger, int a_raw_hi) {
     __shared__ float th[64][65], tl[64][65];
     const int64_t bid = blockIdx.x;
     const int tid = threadIdx.x;
@@ -363,7 +380,14 @@ __global__ void __launch_bounds__(256)
             float* hr = Ah + (int64_t)rr[u] * ldo;
             float* lr = Al + (int64_t)rr[u] * ldo;
             const int64_t c4 = cc[u];
-            if (c4 + 4 <= k) {
+            if (a_raw_hi) {  // A's hi is the raw operand: only lo is written
+                if (c4 + 4 <= k) {
+                    *reinterpret_cast<float4*>(lr + c4) =
+                        make_float4(lo_trunc(x[u].x), lo_trunc(x[u].y), lo_trunc(x[u].z), lo_trunc(x[u].w));
+                } else {
+                    for (int64_t c = c4; c < k; ++c) lr[c] = lo_trunc(xr[c]);
+                }
+            } else if (c4 + 4 <= k) {
                 float4 h, l;
                 split1(x[u].x, h.x, l.x);
                 split1(x[u].y, h.y, l.y);
@@ -942,14 +966,26 @@ fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_
     float* Al = Ah + m * kp;
     float* Bh = Al + m * kp;
     float* Bl = Bh + n * kp;
+    // Raw-hi mode (A/B knob FB_GEMM_AHI_RAW, default 1): A's hi operand is A itself (the tensor core
+    // truncates it to TF32, reading R21) and only lo = rna(a - trunc(a)) is written -- 16 of the
+    // 96 MiB of split traffic at 2048^3; a transposed A is split to exactly those values
+    const bool raw_mode = knobs().gemm_ahi_raw != 0;
+    bool a_raw = false;  // Ah = A (raw) instead of a split hi
     if (ta || tb) {  // transposed operands: A^T stored k x m splits transposing, B^T stored n x k as is
-        FB_TRY(tf32_split_device(ta, ta ? k : m, ta ? m : k, (const float*)A, lda, Ah, Al, kp, st, s));
+        if (ta)
+            FB_TRY(tf32_split_device(1, k, m, (const float*)A, lda, Ah, Al, kp, st, s, raw_mode));
+        else if (raw_mode)
+            FB_TRY(tf32_lo_device(m, k, (const float*)A, lda, Al, kp, s));
+        else
+            FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
+        a_raw = !ta && raw_mode;
         FB_TRY(tf32_split_device(tb ? 0 : 1, tb ? n : k, tb ? k : n, (const float*)B, ldb, Bh, Bl, kp, st, s));
     } else if (knobs().gemm_split2 == 1) {  // A/B knob: 1 = two split launches
         FB_TRY(tf32_split_device(0, m, k, (const float*)A, lda, Ah, Al, kp, st, s));
         FB_TRY(tf32_split_device(1, k, n, (const float*)B, ldb, Bh, Bl, kp, st, s));
     } else if (knobs().gemm_splitv != 1 &&
                m * ((k + 3) / 4) + 1024 < INT32_MAX) {
+        a_raw = raw_mode;
         // default: the wide split (A/B knob FB_GEMM_SPLITV=1: split_both_kernel)
         const int64_t nblk_a = (m * ((k + 3) / 4) + 1023) / 1024;
         const int64_t nblk_b = ((k + 63) / 64) * ((n + 63) / 64);
@@ -959,7 +995,7 @@ fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_
         }
         tf32::split_both_wide_kernel<<<(unsigned)(nblk_a + nblk_b), 256, 0, s>>>(
             (const float*)A, m, k, lda, Ah, Al, (const float*)B, n, ldb, Bh, Bl, kp, nblk_a,
-            knobs().gemm_split_pdl == 1 ? 1 : 0);
+            knobs().gemm_split_pdl == 1 ? 1 : 0, a_raw ? 1 : 0);
         FB_LAUNCH_CHECK("split_both_wide_kernel");
     } else {
         const int a_cblk = (int)((((k + 3) / 4) + 255) / 256);
@@ -984,20 +1020,21 @@ fb_status gemm_ex_device(int dtype, int ta, int tb, int64_t m, int64_t n, int64_
     if (w < 0) w = ((m + 255) / 256) * 8 >= 444 && n > 2048 ? 2048 : 0;
     if (w > 0 && n > w) {
         for (int64_t j0 = 0; j0 < n; j0 += w)
-            FB_TRY(gemm_3xtf32_presplit_device(m, std::min(w, n - j0), k, Ah, Al, kp, Bh + j0 * kp, Bl + j0 * kp, kp,
-                                               (float*)C + j0, ldc, s, (float)alpha, (float)beta));
+            FB_TRY(gemm_3xtf32_presplit_device(m, std::min(w, n - j0), k, a_raw ? (const float*)A : Ah, Al, kp,
+                                               Bh + j0 * kp, Bl + j0 * kp, kp, (float*)C + j0, ldc, s, (float)alpha,
+                                               (float)beta, a_raw ? lda : -1));
         return FB_OK;
     }
-    return gemm_3xtf32_presplit_device(m, n, k, Ah, Al, kp, Bh, Bl, kp, (float*)C, ldc, s, (float)alpha,
-                                       (float)beta);
+    return gemm_3xtf32_presplit_device(m, n, k, a_raw ? (const float*)A : Ah, Al, kp, Bh, Bl, kp, (float*)C, ldc, s,
+                                       (float)alpha, (float)beta, a_raw ? lda : -1);
 }
 
 fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const float* X, int64_t ldx, float* hi,
-                            float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s) {
+                            float* lo, int64_t ldo, const DeviceState* st, cudaStream_t s, bool trunc_hi) {
     if (!transpose) {
         const int64_t chunks = (cols + 3) / 4;
         dim3 g((unsigned)((chunks + 127) / 128), (unsigned)(rows < 8192 ? rows : 8192));
-        tf32::split_rows_kernel<<<g, 128, 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
+        tf32::split_rows_kernel<false><<<g, 128, 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
         FB_LAUNCH_CHECK("split_rows_kernel");
     } else {
         dim3 g2((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
@@ -1005,17 +1042,29 @@ fb_status tf32_split_device(int transpose, int64_t rows, int64_t cols, const flo
             set_error("too many rows for the transposing split grid");
             return FB_ERR_UNSUPPORTED_SIZE;
         }
-        tf32::split_transpose_kernel<<<g2, dim3(32, 8), 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
+        if (trunc_hi)
+            tf32::split_transpose_kernel<true><<<g2, dim3(32, 8), 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
+        else
+            tf32::split_transpose_kernel<false><<<g2, dim3(32, 8), 0, s>>>(X, rows, cols, ldx, hi, lo, ldo);
         FB_LAUNCH_CHECK("split_transpose_kernel");
     }
     return FB_OK;
 }
 
+fb_status tf32_lo_device(int64_t rows, int64_t cols, const float* X, int64_t ldx, float* lo, int64_t ldo,
+                         cudaStream_t s) {
+    const int64_t chunks = (cols + 3) / 4;
+    dim3 g((unsigned)((chunks + 127) / 128), (unsigned)(rows < 8192 ? rows : 8192));
+    tf32::split_rows_kernel<true><<<g, 128, 0, s>>>(X, rows, cols, ldx, nullptr, lo, ldo);
+    FB_LAUNCH_CHECK("split_rows_kernel<lo>");
+    return FB_OK;
+}
+
 fb_status gemm_3xtf32_presplit_device(int64_t m, int64_t n, int64_t k, const float* Ah, const float* Al,
                                       int64_t lda, const float* Bh, const float* Bl, int64_t ldb, float* C,
-                                      int64_t ldc, cudaStream_t s, float alpha, float beta) {
+                                      int64_t ldc, cudaStream_t s, float alpha, float beta, int64_t lda_hi) {
     CUtensorMap mAh, mAl, mBh, mBl;
-    FB_TRY(tf32::make_kmajor_map(&mAh, Ah, m, k, lda, tf32::BM));
+    FB_TRY(tf32::make_kmajor_map(&mAh, Ah, m, k, lda_hi >= 0 ? lda_hi : lda, tf32::BM));
     FB_TRY(tf32::make_kmajor_map(&mAl, Al, m, k, lda, tf32::BM));
     FB_TRY(tf32::make_kmajor_map(&mBh, Bh, n, k, ldb, tf32::BN));
     FB_TRY(tf32::make_kmajor_map(&mBl, Bl, n, k, ldb, tf32::BN));

@@ -91,21 +91,27 @@ def test_f32_padded_leading_dims(fb):
 
 @pytest.mark.parametrize("m,n,k", [(200, 100, 150), (300, 260, 203), (2048, 2048, 2048), (64, 1000, 8)])
 def test_f32_wide_split_bitwise(fb, m, n, k, monkeypatch):
-    """The default operand split (split_both_wide_kernel: flattened float4 chunks of A, 64 x 64
-    tiles of B, ragged k and n) gives C bit for bit equal to the 32 x 32-tile split_both_kernel
-    (knob FB_GEMM_SPLITV=1): same split per element, same GEMM."""
+    """The wide operand split (split_both_wide_kernel: flattened float4 chunks of A, 64 x 64
+    tiles of B, ragged k and n) with RNA hi/lo for A (FB_GEMM_AHI_RAW=0) gives C bit for bit equal
+    to the 32 x 32-tile split_both_kernel (knob FB_GEMM_SPLITV=1): same split per element, same
+    GEMM.  The default (raw A as the hi operand, only lo = rna(a - trunc(a)) written; reading R21)
+    is a different decomposition: within the bar and bitwise deterministic."""
     Ab = torch.from_numpy(synth.real_matrix(m, (k + 3) // 4 * 4, synth.TID_GEMM_A)).cuda()
     Bb = torch.from_numpy(synth.real_matrix(k, (n + 3) // 4 * 4, synth.TID_GEMM_B)).cuda()
     A, B = Ab[:, :k], Bb[:, :n]
+    C2 = fb.matmul(A, B)
+    C3 = fb.matmul(A, B)
+    monkeypatch.setenv("FB_GEMM_AHI_RAW", "0")
     C1 = fb.matmul(A, B)
     torch.cuda.synchronize()
     monkeypatch.setenv("FB_GEMM_SPLITV", "1")
     C0 = fb.matmul(A, B)
     torch.cuda.synchronize()
-    assert torch.equal(C0, C1)
+    assert torch.equal(C0, C1) and torch.equal(C2, C3)
     if m * n * k <= 2 ** 24:
         ref = oracle.matmul(A.cpu().numpy().copy(), B.cpu().numpy().copy())
         assert oracle.rel_l2(C1.cpu().numpy(), ref) < 1e-5
+        assert oracle.rel_l2(C2.cpu().numpy(), ref) < 1e-5
 
 
 @pytest.mark.parametrize("dt", [np.float32, np.float64])
