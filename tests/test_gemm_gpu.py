@@ -159,6 +159,28 @@ def test_deterministic(fb):
     assert np.array_equal(_mm(fb, A, B), _mm(fb, A, B))
 
 
+def test_tc_operand_truncation_probe(fb):
+    """Reading R21 pin (the raw-A-hi default depends on it): fed a raw FP32 operand
+    x = 1 + 2^-11 + 2^-12 (not TF32-exact; round-to-nearest gives 1 + 2^-10, truncation 1.0),
+    kind::tf32 multiplies trunc(x): C = sum over k = 8 of hi(x) * 1 = 8 exactly, never 8 + 2^-7."""
+    m = n = 128
+    k = 8
+    x = np.float32(1 + 2.0 ** -11 + 2.0 ** -12)
+    Ah = torch.full((m, k), float(x), device="cuda")
+    Al = torch.zeros(m, k, device="cuda")
+    Bh = torch.ones(n, k, device="cuda")
+    Bl = torch.zeros(n, k, device="cuda")
+    C = torch.empty(m, n, device="cuda")
+    fb.fb_matmul_3xtf32_presplit(Ah, Al, Bh, Bl, C)
+    torch.cuda.synchronize()
+    assert torch.all(C == 8.0), float(C[0, 0])
+    # and the full path keeps x exactly through hi = trunc(x), lo = rna(x - trunc(x))
+    A = torch.full((m, k), float(x), device="cuda")
+    Cm = fb.matmul(A, torch.ones(k, n, device="cuda"))
+    torch.cuda.synchronize()
+    assert torch.all(Cm == float(8 * np.float64(x))), float(Cm[0, 0])
+
+
 def test_tc_accumulation_rounding_probe(fb):
     """Reading R11 probe: one k-block adds 0.75 ulp(1) to an accumulator holding 1.0.
     RN accumulation gives 1 + 2^-23, RZ gives 1.0.  Recorded, and the K=32768 test below
