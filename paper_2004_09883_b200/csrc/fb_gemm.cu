@@ -645,7 +645,13 @@ constexpr uint32_t STAGE_BYTES = 4 * TILE_BYTES;          // Ahi, Alo, Bhi, Blo 
 constexpr size_t SMEM = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
 constexpr uint32_t ACC_COLS = 256;                        // N of the pair MMA
 constexpr uint32_t TMEM_COLS = 2 * ACC_COLS;              // double-buffered accumulator
-constexpr int KP_BLOCKS = 4;
+#ifndef FB_TF32_KP
+#define FB_TF32_KP 4
+#endif
+// k-blocks (of 32) between RN promotions: every 128 k.  Longer intervals buy nothing and cost
+// accuracy (A/B: 256 k / 512 k: 2048^3 87.8 -> 87.9 / 87.5 us, 8192^3 -0.6 %; K = 32768 error
+// 9.6e-7 -> 1.8e-6 / 3.6e-6)
+constexpr int KP_BLOCKS = FB_TF32_KP;
 
 // NT: N of the pair tile (256, or 240 so that e.g. 2048 columns make 9 tiles and 2048^2 fills 72 of
 // the 74 CTA pairs in one wave); each CTA stages NT / 2 rows of B^T
