@@ -629,13 +629,15 @@ __global__ void __launch_bounds__(NUM_THREADS, 1)
 }
 
 // ------------------------------------------------------------ 2-CTA (cta_group::2) kernel
-// A CTA pair computes a 256 x 256 tile: CTA r stages A rows [m0 + 128 r, +128) and B^T rows
-// [n0 + 128 r, +128) (both 128 x 32 fp32 per k-block, hi and lo), so each SM's shared-memory
+// A CTA pair computes a 256 x NT tile (NT = 256, or 240 where that fills the 74 pairs better):
+// CTA r stages A rows [m0 + 128 r, +128) and B^T rows [n0 + NT/2 r, +NT/2) (x 32 fp32 per
+// k-block, hi and lo; A's hi is A itself in the default raw-hi mode), so each SM's shared-memory
 // path carries half of each operand (the 1-CTA 128x128 form is bound by the
 // smem data path: TMA writes + operand reads exceed the MMA time).  The leader issues
-// tcgen05.mma.cta_group::2 (M = 256, N = 256, K = 8) into TMEM of both CTAs; each CTA's 8
-// epilogue warps promote their 128 rows x 256 columns (two 128-column halves) into RN FP32
-// registers every KP_BLOCKS k-blocks.
+// tcgen05.mma.cta_group::2 (M = 256, N = NT, K = 8) into TMEM of both CTAs; each CTA's 8
+// epilogue warps promote their 128 rows x NT columns (two NT/2-column halves) into RN FP32
+// registers every KP_BLOCKS k-blocks and apply alpha / beta when storing C.  A launch with
+// fewer pairs than tiles runs persistent (FB_GEMM_PERSIST; measured slower, off).
 namespace pair {
 constexpr int BK = 32, STAGES = 3;                         // per-CTA tile halves: 128 x 32
 constexpr int NUM_THREADS = 320;                          // w0 TMA, w1 MMA/TMEM, w2..9 epilogue
