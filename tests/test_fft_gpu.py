@@ -222,11 +222,12 @@ def test_host_variant(fb):
     assert oracle.rel_l2(xh.numpy(), x) < 5e-7
 
 
-@pytest.mark.parametrize("batch", [1, 2, 5])
-def test_host_batch_pipeline(fb, batch):
+@pytest.mark.parametrize("batch,n0,n1", [(1, 512, 256), (2, 512, 256), (5, 512, 256), (3, 256, 256),
+                                         (2, 360, 100), (2, 1000, 24)])
+def test_host_batch_pipeline(fb, batch, n0, n1):
     """Streaming host form: each transform of the batch equals the single-call result bit for
-    bit (same kernels, two device slots on two streams) and the oracle within the gate."""
-    n0, n1 = 512, 256
+    bit (same kernels, two device slots on two streams) and the oracle within the gate -- also
+    for the 256^2 cluster kernel and non-power-of-two sizes (their workspace inside each slot)."""
     xs = np.stack([synth.complex_field(n0, n1, tensor_id=100 + i) for i in range(batch)])
     xb = torch.from_numpy(xs).pin_memory()
     yb = torch.empty_like(xb).pin_memory()
