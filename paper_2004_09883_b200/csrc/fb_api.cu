@@ -49,6 +49,7 @@ static Knobs read_knobs() {
     k.fft_row16k = env_int("FB_FFT_ROW16K", k.fft_row16k);
     k.fft_row16k_cps = env_int("FB_FFT_ROW16K_CPS", k.fft_row16k_cps);
     k.fft_small = env_int("FB_FFT_SMALL", k.fft_small);
+    k.fft_stagger_col = env_int("FB_FFT_STAGGER_COL", k.fft_stagger_col);
     k.fft_mixed = env_int("FB_FFT_MIXED", k.fft_mixed);
     k.fft_mr_small = env_int("FB_FFT_MR_SMALL", k.fft_mr_small);
     k.slab_fused = env_int("FB_SLAB_FUSED", k.slab_fused);

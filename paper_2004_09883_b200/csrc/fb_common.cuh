@@ -64,6 +64,7 @@ struct Knobs {
     int fft_no_pdl = 0, fft_debug = 0, fft_sub = 0;  // FB_FFT_SUB: 0 auto, 1 / 3 forced
     int fft_sub_ilv = 0, fft_col32 = 1, fft_row16k = 1, fft_row16k_cps = 2;
     int fft_mixed = 1, fft_mr_small = 1024;  // 7-smooth non-power-of-two lines as mixed-radix Stockham (0: Bluestein)
+    int fft_stagger_col = 300;  // radix-32 column pass stagger (ns; -1: as FB_FFT_STAGGER); 2048^2: 600 ns 32.68, 300 ns 32.37-32.53, 150 ns 32.39 us
     int fft_small = 16;  // 256 x 256 as one cluster kernel: cluster size 16 (8), 0 = two-pass path
     // multi-GPU (fb_comm.cu)
     int slab_fused = 1;

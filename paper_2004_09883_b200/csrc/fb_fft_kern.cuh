@@ -1763,7 +1763,9 @@ static fb_status launch_col1024(const FftPass& p, const DeviceState* st, cudaStr
         set_error("cuTensorMapEncodeTiled failed for the radix-32 column pass");
         return FB_ERR_CUDA;
     }
-    return launch_pdl(fft_col1024_kernel<0>, dim3((unsigned)grid), dim3(kC32Threads), kC32Smem, s, p, tin, tout,
+    FftPass pk = p;
+    if (knobs().fft_stagger_col >= 0) pk.stagger_ns = knobs().fft_stagger_col;  // A/B knob
+    return launch_pdl(fft_col1024_kernel<0>, dim3((unsigned)grid), dim3(kC32Threads), kC32Smem, s, pk, tin, tout,
                       (const float2*)st->twiddles, ngroups);
 }
 
