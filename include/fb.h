@@ -117,9 +117,11 @@ fb_status fb_irfft2d(const void* y, void* x, int64_t n0, int64_t n1, void* ws, s
 /* ------------------------------------------------------------------ matrix block
  * C[m][n] = A[m][k] * B[k][n]  (row-major, leading dimensions in ELEMENTS, C overwritten).
  * FB_F64: IEEE FP64 (DMMA tensor-core FMAs, RN); accuracy rel-L2 <= 1e-12.
- * FB_F32: FP32 via 3xTF32 on tcgen05 tensor cores (hi*hi + hi*lo + lo*hi with RN-split
- *         operands, FP32 accumulation in TMEM); accuracy rel-L2 <= 1e-5 (reading R11).
- *         Not bitwise equal to an FP32 SIMT GEMM.
+ * FB_F32: FP32 via 3xTF32 on tcgen05 tensor cores (hi*hi + hi*lo + lo*hi; B split RN into
+ *         hi/lo, A used raw as hi -- the tensor core truncates it to TF32, reading R21 -- with
+ *         lo = rn(a - trunc(a)); FP32 accumulation in TMEM promoted to RN registers every
+ *         128 k); accuracy rel-L2 <= 1e-5 (reading R11).  Bitwise deterministic for a fixed
+ *         shape; not bitwise equal to an FP32 SIMT GEMM.
  * m, n, k >= 1 (any value: ragged edges are handled).  A, B, C 16-byte aligned;
  * lda, ldb, ldc >= the row width and lda*esize, ldb*esize, ldc*esize multiples of 16 B.
  * ws: device workspace of fb_matmul_workspace_bytes(...) bytes (FP32: the TF32 hi/lo
