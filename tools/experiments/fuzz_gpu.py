@@ -17,7 +17,7 @@ rng = random.Random(int(sys.argv[2]) if len(sys.argv) > 2 else 7)
 torch.cuda.set_device(0)
 fb.fb_init(0)
 fails = []
-counts = {"fft2d": 0, "gemm": 0, "bf16": 0}
+counts = {"fft2d": 0, "gemm": 0, "bf16": 0, "fft1d": 0, "rfft2d": 0, "slab": 0}
 
 
 def rel(a, b):
@@ -77,6 +77,39 @@ for case in range(N):
             counts["gemm"] += 1
             if not e < (1e-5 if dt == torch.float32 else 1e-12):
                 fails.append(("gemm", str(dt), m, n, k, ta, tb, alpha, beta, e))
+        elif kind < 0.90:
+            sub = rng.random()
+            if sub < 0.4:  # batched 1D
+                n, b = 2 ** rng.randint(0, 14), rng.randint(1, 300)
+                x = (np.random.default_rng(case).standard_normal((b, n)) +
+                     1j * np.random.default_rng(case + 2).standard_normal((b, n))).astype(np.complex64)
+                y = fb.fft1d(torch.from_numpy(x).cuda()).cpu().numpy()
+                e = rel(y, np.fft.fft(x.astype(np.complex128), axis=1))
+                counts["fft1d"] += 1
+                if not e < 1e-5 * max(1.0, np.log2(n)):
+                    fails.append(("fft1d", b, n, e))
+            elif sub < 0.7:  # real input
+                n0, n1 = 2 ** rng.randint(0, 11), 2 ** rng.randint(1, 11)
+                x = np.random.default_rng(case).standard_normal((n0, n1)).astype(np.float32)
+                y = fb.rfft2d(torch.from_numpy(x).cuda())
+                z = fb.irfft2d(y, n1).cpu().numpy()
+                e, ei = rel(y.cpu().numpy(), np.fft.rfft2(x.astype(np.float64))), rel(z, x)
+                counts["rfft2d"] += 1
+                if not (e < 1e-5 * max(1.0, np.log2(n0 * n1)) and ei < 1e-5 * max(1.0, np.log2(n0 * n1))):
+                    fails.append(("rfft2d", n0, n1, e, ei))
+            else:  # slab model, P virtual ranks
+                P = rng.choice([1, 2, 4, 8])
+                n0, n1 = 2 ** rng.randint(3, 12), 2 ** rng.randint(3, 12)
+                x = (np.random.default_rng(case).standard_normal((n0, n1)) +
+                     1j * np.random.default_rng(case + 3).standard_normal((n0, n1))).astype(np.complex64)
+                xd = torch.from_numpy(x).cuda()
+                yd = torch.empty(n0 * n1, dtype=torch.complex64, device="cuda")
+                fb.fb_fft2d_slab_model(P, xd, yd, n0, n1)
+                y = yd.view(P, n0, n1 // P).permute(1, 0, 2).reshape(n0, n1).cpu().numpy()
+                e = rel(y, np.fft.fft2(x.astype(np.complex128)))
+                counts["slab"] += 1
+                if not e < 1e-5 * max(1.0, np.log2(n0 * n1)):
+                    fails.append(("slab", P, n0, n1, e))
         else:
             m = rng.randint(1, 1200)
             n = rng.randint(1, 1200) // 8 * 8 or 8
